@@ -1,0 +1,86 @@
+/*
+ * hebatch_b200 -- C ABI of the B200-native homomorphic-operator library.
+ *
+ * This is the drop-in boundary for the hot path of the reference package `hebatch`
+ * (/root/reference/pkg/src/hebatch): every entry point replaces one element kernel that the
+ * reference runs through ExecutionBackend.run (backends.py:28) on top of gmpy2.  The reference has
+ * no FFI of its own (pure Python over gmpy2), so the binding a maintainer adds is the ctypes stub
+ * shown in INTEGRATION.md.
+ *
+ * Conventions
+ *   - Every big integer is an array of little-endian 32-bit words.  Plaintext residues (mod n) use
+ *     hb_pt_words(ctx) words, ciphertexts (mod n^2) use hb_ct_words(ctx) words.  For key sizes that
+ *     are multiples of 16 bits this is byte-for-byte the HAFB wire payload (bufferpool.py:231-330).
+ *   - Batches are dense arrays: element i starts at word i * words.
+ *   - Functions whose names do not end in _host take DEVICE pointers and enqueue work on `stream`
+ *     (a cudaStream_t passed as void*; NULL = the legacy default stream).  They never synchronise and
+ *     never allocate host memory; scratch comes from the stream-ordered allocator.
+ *   - *_host functions take HOST pointers, stage through pinned buffers on side streams (chunked,
+ *     copy/compute overlapped) and return when the result is in the caller's buffer.
+ *   - Return value: 0 on success, negative hb_status on failure; hb_last_error() gives the text
+ *     (thread-local).  There is no CPU fallback: without a usable CUDA device every call fails.
+ */
+#ifndef HEBATCH_B200_H
+#define HEBATCH_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hb_ctx hb_ctx;
+
+enum hb_status {
+  HB_OK = 0,
+  HB_ERR_ARG = -1,        /* bad argument (null pointer, even modulus, size mismatch, ...) */
+  HB_ERR_CUDA = -2,       /* CUDA runtime failure */
+  HB_ERR_UNSUPPORTED = -3,/* key size beyond the instantiated limb configurations */
+  HB_ERR_NOPRIVATE = -4,  /* decrypt requested on a context without the private part */
+  HB_ERR_NOTUNIT = -5     /* modular inverse of a non-unit (gmpy2.invert raises ZeroDivisionError) */
+};
+
+const char* hb_last_error(void);
+/* Library version and the GPU architecture it was compiled for ("sm_100a"). */
+const char* hb_version(void);
+
+/* ---- key context ------------------------------------------------------------------------------
+ * Replaces the per-call `common` tuples of operators.py (:40,45,50,66,71) and the cached values of
+ * paillier.PublicKey (:39-66) / PrivateKey (:69-107).  n is key_bits wide; n^2, Montgomery constants
+ * and the exponent schedule for r^n are derived here, once.                                        */
+int hb_ctx_create(hb_ctx** out, const uint32_t* n_words, int n_nwords, int device);
+/* Private part for CRT decryption (paillier.py:94-98): primes p, q and hp, hq, q^-1 mod p, each as
+ * `nwords` little-endian words. */
+int hb_ctx_set_private(hb_ctx* ctx, const uint32_t* p, const uint32_t* q, const uint32_t* hp,
+                       const uint32_t* hq, const uint32_t* q_inv_p, int nwords);
+void hb_ctx_destroy(hb_ctx* ctx);
+int hb_pt_words(const hb_ctx* ctx);   /* words per plaintext residue  = ceil(key_bits / 32)           */
+int hb_ct_words(const hb_ctx* ctx);   /* words per ciphertext         = ceil(ceil(2*key_bits/8) / 4)  */
+int hb_key_bits(const hb_ctx* ctx);
+
+/* ---- element operators (device pointers) --------------------------------------------------------*/
+/* _k_encrypt, operators.py:39-41:  out[i] = (1 + m[i]*n) * r[i]^n mod n^2.   m, r: pt words. */
+int hb_encrypt(hb_ctx* ctx, const uint32_t* m, const uint32_t* r, uint32_t* out, int64_t count, void* stream);
+/* _k_obfuscate, operators.py:44-46: out[i] = c[i] * r[i]^n mod n^2. */
+int hb_obfuscate(hb_ctx* ctx, const uint32_t* c, const uint32_t* r, uint32_t* out, int64_t count, void* stream);
+/* _k_decrypt, operators.py:49-56 (CRT form of paillier.py:201-209): m_out[i] in [0, n). */
+int hb_decrypt(hb_ctx* ctx, const uint32_t* c, uint32_t* m_out, int64_t count, void* stream);
+/* _k_add, operators.py:70-72: out[i] = a[i] * b[i] mod n^2.  b_stride_zero != 0 broadcasts b[0]. */
+int hb_mulmod(hb_ctx* ctx, const uint32_t* a, const uint32_t* b, uint32_t* out, int64_t count,
+              int b_broadcast, void* stream);
+/* batch_add with a plaintext operand, operators.py:209-212: out[i] = a[i] * (1 + m[i]*n) mod n^2. */
+int hb_lift_mulmod(hb_ctx* ctx, const uint32_t* a, const uint32_t* m, uint32_t* out, int64_t count,
+                   int m_broadcast, void* stream);
+
+/* ---- host-buffer convenience path (pinned staging, side streams) --------------------------------*/
+int hb_encrypt_host(hb_ctx* ctx, const uint32_t* m, const uint32_t* r, uint32_t* out, int64_t count);
+int hb_decrypt_host(hb_ctx* ctx, const uint32_t* c, uint32_t* m_out, int64_t count);
+
+/* ---- instrumentation ----------------------------------------------------------------------------*/
+/* Number of kernels this library has launched since load (all contexts). */
+int64_t hb_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HEBATCH_B200_H */

@@ -1,0 +1,401 @@
+// C ABI of the B200 homomorphic-operator library (include/hebatch_b200.h).
+#include <cstdio>
+#include <cstring>
+#include <atomic>
+#include <mutex>
+#include <string>
+#include <vector>
+#include <cuda_runtime.h>
+
+#include "../../include/hebatch_b200.h"
+#include "hb_host.h"
+#include "hb_kernels.cuh"
+
+using hbh::Big;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<long long> g_launches{0};
+
+int fail(int code, const std::string& msg) { g_err = msg; return code; }
+#define CU(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) \
+  return fail(HB_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); } while (0)
+
+// Instantiated limb configurations, ordered by digit count L = LPT * TPI (capacity 29*L bits).
+struct Cfg { int lpt, tpi; };
+const Cfg kCfgs[] = {{9, 4}, {18, 4}, {27, 4}, {18, 8}, {27, 8}};
+constexpr int kNumCfg = 5;
+constexpr int kMargin = 6;   // R must exceed the modulus by this many bits
+
+int pick_cfg(int bits) {
+  for (int i = 0; i < kNumCfg; i++)
+    if (29 * kCfgs[i].lpt * kCfgs[i].tpi >= bits + kMargin) return i;
+  return -1;
+}
+int window_for(int ebits) { return ebits >= 768 ? 5 : ebits >= 160 ? 4 : ebits >= 24 ? 3 : 2; }
+
+// Builder of the per-context constant block (one device allocation).
+struct ConstBlock {
+  std::vector<uint32_t> host;
+  size_t add(const std::vector<uint32_t>& v) {
+    size_t off = host.size();
+    host.insert(host.end(), v.begin(), v.end());
+    while (host.size() % 4) host.push_back(0);
+    return off;
+  }
+};
+
+struct ModOff { size_t n, r1, r2; uint32_t np; };
+
+ModOff add_modulus(ConstBlock& cb, const Big& mod, int L) {
+  ModOff m;
+  Big one{1};
+  m.n = cb.add(hbh::to_digits(mod, L));
+  m.r1 = cb.add(hbh::to_digits(hbh::shl_mod(one, 29L * L, mod), L));
+  m.r2 = cb.add(hbh::to_digits(hbh::shl_mod(one, 2 * 29L * L, mod), L));
+  m.np = hbh::neg_inv29(mod[0]);
+  return m;
+}
+
+}  // namespace
+
+struct hb_ctx {
+  int device = 0;
+  int sms = 0;
+  int key_bits = 0, wn = 0, wc = 0;
+  Big n, n2;
+  // public part
+  int cfg_pub = -1;
+  uint32_t* d_pub = nullptr;
+  ModOff mod_n2;
+  size_t off_nR = 0, off_prog_n = 0;
+  int nprog_n = 0, slots_n = 0;
+  // private part
+  bool has_private = false;
+  int cfg_priv = -1;
+  uint32_t* d_priv = nullptr;
+  struct Half { ModOff s2, s1; size_t hiR2, hsR, prog; int nprog; } half[2];
+  size_t off_qinvR = 0, off_qR = 0;
+  ModOff mod_n_priv;
+  int slots_priv = 0;
+  // host-path staging
+  std::mutex mu;
+};
+
+namespace {
+
+hb::ModDev dev_mod(const uint32_t* base, const ModOff& m) {
+  return hb::ModDev{base + m.n, base + m.r1, base + m.r2, m.np};
+}
+
+struct Launch { int blocks; int threads; size_t smem; long nwarps; };
+Launch plan(const hb_ctx* ctx, int cfg, long count) {
+  const int tpi = kCfgs[cfg].tpi, lpt = kCfgs[cfg].lpt;
+  const int ipw = 32 / tpi;
+  long ntiles = (count + ipw - 1) / ipw;
+  long blocks = (ntiles + 3) / 4;
+  long maxb = (long)ctx->sms * hb::blocks_per_sm(lpt);
+  if (blocks > maxb) blocks = maxb;
+  if (blocks < 1) blocks = 1;
+  Launch l;
+  l.blocks = (int)blocks;
+  l.threads = 128;
+  l.smem = (size_t)4 * ipw * (lpt * tpi + 2) * sizeof(uint32_t);
+  l.nwarps = blocks * 4;
+  return l;
+}
+
+#define HB_DISPATCH(cfg, KERNEL, launch, stream, args)                                           \
+  switch (cfg) {                                                                                 \
+    case 0: hb::KERNEL<9, 4><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break;  \
+    case 1: hb::KERNEL<18, 4><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break; \
+    case 2: hb::KERNEL<27, 4><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break; \
+    case 3: hb::KERNEL<18, 8><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break; \
+    case 4: hb::KERNEL<27, 8><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break; \
+    default: return fail(HB_ERR_UNSUPPORTED, "no limb configuration");                            \
+  }                                                                                              \
+  g_launches++;
+
+int encrypt_common(hb_ctx* ctx, const uint32_t* m, const uint32_t* c, const uint32_t* r, uint32_t* out,
+                   int64_t count, int mode, void* stream_) {
+  if (!ctx || !r || !out || (mode == 0 ? !m : !c)) return fail(HB_ERR_ARG, "null pointer");
+  if (count < 0) return fail(HB_ERR_ARG, "negative count");
+  if (count == 0) return HB_OK;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  CU(cudaSetDevice(ctx->device));
+  const int cfg = ctx->cfg_pub;
+  Launch l = plan(ctx, cfg, count);
+  const long stride = (long)(ctx->slots_n + 1) * kCfgs[cfg].lpt * 32;
+  uint32_t* tbl = nullptr;
+  CU(cudaMallocAsync(&tbl, (size_t)stride * l.nwarps * sizeof(uint32_t), stream));
+  hb::EncArgs A;
+  A.mod = dev_mod(ctx->d_pub, ctx->mod_n2);
+  A.nR = ctx->d_pub + ctx->off_nR;
+  A.prog = ctx->d_pub + ctx->off_prog_n;
+  A.nprog = ctx->nprog_n;
+  A.tbl = tbl;
+  A.tbl_stride = stride;
+  A.m = m; A.c = c; A.r = r; A.out = out;
+  A.count = count; A.wn = ctx->wn; A.wc = ctx->wc; A.mode = mode;
+  HB_DISPATCH(cfg, k_encrypt, l, stream, A)
+  CU(cudaGetLastError());
+  CU(cudaFreeAsync(tbl, stream));
+  return HB_OK;
+}
+
+int mulmod_common(hb_ctx* ctx, const uint32_t* a, const uint32_t* b, uint32_t* out, int64_t count,
+                  int lift, int bcast, void* stream_) {
+  if (!ctx || !a || !b || !out) return fail(HB_ERR_ARG, "null pointer");
+  if (count < 0) return fail(HB_ERR_ARG, "negative count");
+  if (count == 0) return HB_OK;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  CU(cudaSetDevice(ctx->device));
+  const int cfg = ctx->cfg_pub;
+  Launch l = plan(ctx, cfg, count);
+  hb::MulArgs A;
+  A.mod = dev_mod(ctx->d_pub, ctx->mod_n2);
+  A.nR = ctx->d_pub + ctx->off_nR;
+  A.a = a; A.b = b; A.out = out; A.count = count; A.wn = ctx->wn; A.wc = ctx->wc;
+  A.lift = lift; A.b_broadcast = bcast;
+  HB_DISPATCH(cfg, k_mulmod, l, stream, A)
+  CU(cudaGetLastError());
+  return HB_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hb_last_error(void) { return g_err.c_str(); }
+const char* hb_version(void) { return "hebatch_b200 0.1 (sm_100a)"; }
+int64_t hb_launch_count(void) { return g_launches.load(); }
+
+int hb_ctx_create(hb_ctx** out, const uint32_t* n_words, int n_nwords, int device) {
+  if (!out || !n_words || n_nwords <= 0) return fail(HB_ERR_ARG, "null pointer");
+  Big n = hbh::from_words(n_words, n_nwords);
+  if (hbh::bitlen(n) < 3 || !(n[0] & 1)) return fail(HB_ERR_ARG, "modulus must be odd and >= 5");
+  int ndev = 0;
+  CU(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(HB_ERR_CUDA, "no such CUDA device");
+  CU(cudaSetDevice(device));
+  hb_ctx* ctx = new hb_ctx();
+  ctx->device = device;
+  cudaDeviceProp prop;
+  cudaError_t e = cudaGetDeviceProperties(&prop, device);
+  if (e != cudaSuccess) { delete ctx; return fail(HB_ERR_CUDA, cudaGetErrorString(e)); }
+  ctx->sms = prop.multiProcessorCount;
+  ctx->n = n;
+  ctx->n2 = hbh::mul(n, n);
+  ctx->key_bits = hbh::bitlen(n);
+  ctx->wn = (ctx->key_bits + 31) / 32;
+  ctx->wc = ((2 * ctx->key_bits + 7) / 8 + 3) / 4;
+  ctx->cfg_pub = pick_cfg(hbh::bitlen(ctx->n2));
+  if (ctx->cfg_pub < 0) { delete ctx; return fail(HB_ERR_UNSUPPORTED, "key too large for the instantiated limb configurations"); }
+  const int L = kCfgs[ctx->cfg_pub].lpt * kCfgs[ctx->cfg_pub].tpi;
+  ConstBlock cb;
+  ctx->mod_n2 = add_modulus(cb, ctx->n2, L);
+  ctx->off_nR = cb.add(hbh::to_digits(hbh::shl_mod(n, 29L * L, ctx->n2), L));
+  std::vector<uint32_t> prog = hbh::build_program(n, window_for(ctx->key_bits), &ctx->slots_n);
+  ctx->nprog_n = (int)prog.size();
+  ctx->off_prog_n = cb.add(prog);
+  e = cudaMalloc(&ctx->d_pub, cb.host.size() * sizeof(uint32_t));
+  if (e == cudaSuccess) e = cudaMemcpy(ctx->d_pub, cb.host.data(), cb.host.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) { delete ctx; return fail(HB_ERR_CUDA, cudaGetErrorString(e)); }
+  *out = ctx;
+  return HB_OK;
+}
+
+int hb_ctx_set_private(hb_ctx* ctx, const uint32_t* p_, const uint32_t* q_, const uint32_t* hp_,
+                       const uint32_t* hq_, const uint32_t* qinv_, int nwords) {
+  if (!ctx || !p_ || !q_ || !hp_ || !hq_ || !qinv_ || nwords <= 0) return fail(HB_ERR_ARG, "null pointer");
+  Big p = hbh::from_words(p_, nwords), q = hbh::from_words(q_, nwords);
+  Big hs[2] = {hbh::from_words(hp_, nwords), hbh::from_words(hq_, nwords)};
+  Big qinv = hbh::from_words(qinv_, nwords);
+  if (hbh::cmp(hbh::mul(p, q), ctx->n) != 0) return fail(HB_ERR_ARG, "p * q does not match n");
+  if (!(p[0] & 1) || !(q[0] & 1)) return fail(HB_ERR_ARG, "primes must be odd");
+  if (hbh::cmp(hs[0], p) >= 0 || hbh::cmp(hs[1], q) >= 0 || hbh::cmp(qinv, p) >= 0) return fail(HB_ERR_ARG, "private constants out of range");
+  CU(cudaSetDevice(ctx->device));
+  Big s[2] = {p, q};
+  Big s2[2] = {hbh::mul(p, p), hbh::mul(q, q)};
+  const int wlo = ctx->wc / 2;
+  int need = std::max(std::max(hbh::bitlen(s2[0]), hbh::bitlen(s2[1])), ctx->key_bits);
+  need = std::max(need, 32 * std::max(wlo, ctx->wc - wlo));
+  int cfg = pick_cfg(need);
+  if (cfg < 0) return fail(HB_ERR_UNSUPPORTED, "key too large for the instantiated limb configurations");
+  const int L = kCfgs[cfg].lpt * kCfgs[cfg].tpi;
+  ConstBlock cb;
+  Big one{1};
+  int slots = 0;
+  for (int h = 0; h < 2; h++) {
+    ctx->half[h].s2 = add_modulus(cb, s2[h], L);
+    ctx->half[h].s1 = add_modulus(cb, s[h], L);
+    ctx->half[h].hiR2 = cb.add(hbh::to_digits(hbh::shl_mod(one, 32L * wlo + 2 * 29L * L, s2[h]), L));
+    ctx->half[h].hsR = cb.add(hbh::to_digits(hbh::shl_mod(hs[h], 29L * L, s[h]), L));
+    Big e = hbh::sub_small(s[h], 1);
+    int used = 0;
+    std::vector<uint32_t> prog = hbh::build_program(e, window_for(hbh::bitlen(e)), &used);
+    slots = std::max(slots, used);
+    ctx->half[h].nprog = (int)prog.size();
+    ctx->half[h].prog = cb.add(prog);
+  }
+  ctx->off_qinvR = cb.add(hbh::to_digits(hbh::shl_mod(qinv, 29L * L, p), L));
+  ctx->mod_n_priv = add_modulus(cb, ctx->n, L);
+  ctx->off_qR = cb.add(hbh::to_digits(hbh::shl_mod(q, 29L * L, ctx->n), L));
+  ctx->slots_priv = slots;
+  if (ctx->d_priv) { cudaFree(ctx->d_priv); ctx->d_priv = nullptr; }
+  CU(cudaMalloc(&ctx->d_priv, cb.host.size() * sizeof(uint32_t)));
+  CU(cudaMemcpy(ctx->d_priv, cb.host.data(), cb.host.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+  ctx->cfg_priv = cfg;
+  ctx->has_private = true;
+  return HB_OK;
+}
+
+void hb_ctx_destroy(hb_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->d_pub) cudaFree(ctx->d_pub);
+  if (ctx->d_priv) cudaFree(ctx->d_priv);
+  delete ctx;
+}
+
+int hb_pt_words(const hb_ctx* ctx) { return ctx ? ctx->wn : 0; }
+int hb_ct_words(const hb_ctx* ctx) { return ctx ? ctx->wc : 0; }
+int hb_key_bits(const hb_ctx* ctx) { return ctx ? ctx->key_bits : 0; }
+
+int hb_encrypt(hb_ctx* ctx, const uint32_t* m, const uint32_t* r, uint32_t* out, int64_t count, void* stream) {
+  return encrypt_common(ctx, m, nullptr, r, out, count, 0, stream);
+}
+int hb_obfuscate(hb_ctx* ctx, const uint32_t* c, const uint32_t* r, uint32_t* out, int64_t count, void* stream) {
+  return encrypt_common(ctx, nullptr, c, r, out, count, 1, stream);
+}
+int hb_mulmod(hb_ctx* ctx, const uint32_t* a, const uint32_t* b, uint32_t* out, int64_t count,
+              int b_broadcast, void* stream) {
+  return mulmod_common(ctx, a, b, out, count, 0, b_broadcast, stream);
+}
+int hb_lift_mulmod(hb_ctx* ctx, const uint32_t* a, const uint32_t* m, uint32_t* out, int64_t count,
+                   int m_broadcast, void* stream) {
+  return mulmod_common(ctx, a, m, out, count, 1, m_broadcast, stream);
+}
+
+int hb_decrypt(hb_ctx* ctx, const uint32_t* c, uint32_t* m_out, int64_t count, void* stream_) {
+  if (!ctx || !c || !m_out) return fail(HB_ERR_ARG, "null pointer");
+  if (!ctx->has_private) return fail(HB_ERR_NOPRIVATE, "context has no private key");
+  if (count < 0) return fail(HB_ERR_ARG, "negative count");
+  if (count == 0) return HB_OK;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  CU(cudaSetDevice(ctx->device));
+  const int cfg = ctx->cfg_priv;
+  Launch l = plan(ctx, cfg, count);
+  const long stride = (long)(ctx->slots_priv + 1) * kCfgs[cfg].lpt * 32;
+  uint32_t* tbl = nullptr;
+  CU(cudaMallocAsync(&tbl, (size_t)stride * l.nwarps * sizeof(uint32_t), stream));
+  const uint32_t* base = ctx->d_priv;
+  hb::DecArgs A;
+  for (int h = 0; h < 2; h++) {
+    A.half[h].s2 = dev_mod(base, ctx->half[h].s2);
+    A.half[h].s1 = dev_mod(base, ctx->half[h].s1);
+    A.half[h].hiR2 = base + ctx->half[h].hiR2;
+    A.half[h].hsR = base + ctx->half[h].hsR;
+    A.half[h].prog = base + ctx->half[h].prog;
+    A.half[h].nprog = ctx->half[h].nprog;
+  }
+  A.qinvR = base + ctx->off_qinvR;
+  A.modn = dev_mod(base, ctx->mod_n_priv);
+  A.qR = base + ctx->off_qR;
+  A.tbl = tbl; A.tbl_stride = stride; A.stash_slot = ctx->slots_priv;
+  A.c = c; A.out = m_out; A.count = count; A.wn = ctx->wn; A.wc = ctx->wc;
+  HB_DISPATCH(cfg, k_decrypt, l, stream, A)
+  CU(cudaGetLastError());
+  CU(cudaFreeAsync(tbl, stream));
+  return HB_OK;
+}
+
+// ---- host-buffer path: pinned staging + two side streams, chunks double-buffered ------------------
+namespace {
+struct Stage {
+  cudaStream_t s = nullptr;
+  uint32_t *h_in0 = nullptr, *h_in1 = nullptr, *h_out = nullptr;
+  uint32_t *d_in0 = nullptr, *d_in1 = nullptr, *d_out = nullptr;
+  cudaEvent_t done = nullptr;
+};
+}  // namespace
+
+static int host_pipeline(hb_ctx* ctx, int kind, const uint32_t* in0, const uint32_t* in1, uint32_t* out,
+                         int64_t count) {
+  // kind 0: encrypt(in0 = m [wn], in1 = r [wn]) -> out [wc];  kind 1: decrypt(in0 = c [wc]) -> out [wn]
+  if (!ctx || !in0 || !out || (kind == 0 && !in1)) return fail(HB_ERR_ARG, "null pointer");
+  if (count <= 0) return count == 0 ? HB_OK : fail(HB_ERR_ARG, "negative count");
+  std::lock_guard<std::mutex> lock(ctx->mu);
+  CU(cudaSetDevice(ctx->device));
+  const size_t w_in0 = kind == 0 ? ctx->wn : ctx->wc, w_in1 = kind == 0 ? ctx->wn : 0;
+  const size_t w_out = kind == 0 ? ctx->wc : ctx->wn;
+  const int cfg = kind == 0 ? ctx->cfg_pub : ctx->cfg_priv;
+  if (cfg < 0) return fail(HB_ERR_NOPRIVATE, "context has no private key");
+  // four full waves of the persistent grid per chunk, so chunking costs no tail
+  const int64_t wave = (int64_t)ctx->sms * 4 * hb::blocks_per_sm(kCfgs[cfg].lpt) * (32 / kCfgs[cfg].tpi);
+  const int64_t chunk = std::min<int64_t>(count, 4 * wave);
+  Stage st[2];
+  int rc = HB_OK;
+  auto cleanup = [&]() {
+    for (auto& s : st) {
+      if (s.s) cudaStreamSynchronize(s.s);
+      if (s.h_in0) cudaFreeHost(s.h_in0);
+      if (s.h_in1) cudaFreeHost(s.h_in1);
+      if (s.h_out) cudaFreeHost(s.h_out);
+      if (s.d_in0) cudaFree(s.d_in0);
+      if (s.d_in1) cudaFree(s.d_in1);
+      if (s.d_out) cudaFree(s.d_out);
+      if (s.done) cudaEventDestroy(s.done);
+      if (s.s) cudaStreamDestroy(s.s);
+    }
+  };
+#define CUX(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { cleanup(); \
+  return fail(HB_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); } } while (0)
+  const int nst = count > chunk ? 2 : 1;
+  for (int i = 0; i < nst; i++) {
+    CUX(cudaStreamCreateWithFlags(&st[i].s, cudaStreamNonBlocking));
+    CUX(cudaEventCreateWithFlags(&st[i].done, cudaEventDisableTiming));
+    CUX(cudaMallocHost(&st[i].h_in0, chunk * w_in0 * 4));
+    CUX(cudaMalloc(&st[i].d_in0, chunk * w_in0 * 4));
+    if (w_in1) { CUX(cudaMallocHost(&st[i].h_in1, chunk * w_in1 * 4)); CUX(cudaMalloc(&st[i].d_in1, chunk * w_in1 * 4)); }
+    CUX(cudaMallocHost(&st[i].h_out, chunk * w_out * 4));
+    CUX(cudaMalloc(&st[i].d_out, chunk * w_out * 4));
+  }
+  struct Pending { int64_t off, n; bool active; } pend[2] = {{0, 0, false}, {0, 0, false}};
+  const int64_t nchunks = (count + chunk - 1) / chunk;
+  for (int64_t i = 0; i < nchunks + nst; i++) {
+    const int which = (int)(i % nst);
+    Stage& s = st[which];
+    if (pend[which].active) {   // drain the chunk this stage submitted nst iterations ago
+      CUX(cudaEventSynchronize(s.done));
+      memcpy(out + pend[which].off * w_out, s.h_out, pend[which].n * w_out * 4);
+      pend[which].active = false;
+    }
+    if (i >= nchunks) continue;
+    const int64_t off = i * chunk, n = std::min(chunk, count - off);
+    memcpy(s.h_in0, in0 + off * w_in0, n * w_in0 * 4);
+    CUX(cudaMemcpyAsync(s.d_in0, s.h_in0, n * w_in0 * 4, cudaMemcpyHostToDevice, s.s));
+    if (w_in1) {
+      memcpy(s.h_in1, in1 + off * w_in1, n * w_in1 * 4);
+      CUX(cudaMemcpyAsync(s.d_in1, s.h_in1, n * w_in1 * 4, cudaMemcpyHostToDevice, s.s));
+    }
+    rc = kind == 0 ? hb_encrypt(ctx, s.d_in0, s.d_in1, s.d_out, n, s.s) : hb_decrypt(ctx, s.d_in0, s.d_out, n, s.s);
+    if (rc != HB_OK) { cleanup(); return rc; }
+    CUX(cudaMemcpyAsync(s.h_out, s.d_out, n * w_out * 4, cudaMemcpyDeviceToHost, s.s));
+    CUX(cudaEventRecord(s.done, s.s));
+    pend[which] = {off, n, true};
+  }
+#undef CUX
+  cleanup();
+  return HB_OK;
+}
+
+int hb_encrypt_host(hb_ctx* ctx, const uint32_t* m, const uint32_t* r, uint32_t* out, int64_t count) {
+  return host_pipeline(ctx, 0, m, r, out, count);
+}
+int hb_decrypt_host(hb_ctx* ctx, const uint32_t* c, uint32_t* m_out, int64_t count) {
+  return host_pipeline(ctx, 1, c, nullptr, m_out, count);
+}
+
+}  // extern "C"

@@ -1,0 +1,272 @@
+// Batched Paillier kernels for sm_100a built on the warp-cooperative Montgomery core (mont.cuh).
+//
+// One instance (one ciphertext / plaintext element) is owned by a group of TPI lanes; a warp holds
+// 32/TPI instances ("a tile") and a grid-stride loop walks the tiles.  All instances of a launch
+// share the modulus and, for encrypt / obfuscate / decrypt, the exponent, so control flow is uniform
+// across the grid: the exponent is compiled on the host into a flat op program (sliding window over
+// odd powers) that every warp replays.  Window tables live in a per-warp scratch tile in global memory
+// laid out [entry][digit][lane] so each access is one coalesced 128-byte row.
+//
+// Reference semantics (file:line under /root/reference/pkg/src/hebatch):
+//   k_encrypt   operators.py:39-46   (1 + m n) r^n mod n^2   |   c r^n mod n^2
+//   k_decrypt   operators.py:49-56   CRT decryption
+//   k_mulmod    operators.py:70-72   a b mod n^2 (optionally b = 1 + m n, operators.py:211)
+#pragma once
+#include "mont.cuh"
+
+namespace hb {
+
+struct ModDev {
+  const uint32_t* n;    // modulus digits (L)
+  const uint32_t* r1;   // R mod n
+  const uint32_t* r2;   // R^2 mod n
+  uint32_t np;          // -n^-1 mod 2^29
+};
+
+// op word of the exponent program: kind | src << 8 | dst << 16
+enum : uint32_t { OP_SQR = 0, OP_MUL = 1, OP_LOAD = 2, OP_KEEP = 3, OP_NODST = 0xFF };
+
+// Resident 128-thread blocks per SM the kernels are compiled for (register budget 128 or 168).
+__host__ __device__ constexpr int blocks_per_sm(int lpt) { return lpt > 20 ? 3 : 4; }
+
+template <int LPT>
+__device__ __forceinline__ void tile_store(uint32_t* tw, int e, const uint32_t (&x)[LPT]) {
+  int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 0; k < LPT; k++) tw[(e * LPT + k) * 32 + lane] = x[k];
+}
+template <int LPT>
+__device__ __forceinline__ void tile_load(const uint32_t* tw, int e, uint32_t (&x)[LPT]) {
+  int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 0; k < LPT; k++) x[k] = tw[(e * LPT + k) * 32 + lane];
+}
+
+// Replays an op program on x (Montgomery form in, Montgomery form out).  Single mul call site.
+template <int LPT, int TPI>
+__device__ __forceinline__ void run_prog(const Mont<LPT, TPI>& mt, uint32_t (&x)[LPT],
+                                         const uint32_t* __restrict__ prog, int nprog, uint32_t* tw) {
+#pragma unroll 1
+  for (int i = 0; i < nprog; i++) {
+    uint32_t op = prog[i];
+    uint32_t kind = op & 0xFF, src = (op >> 8) & 0xFF, dst = (op >> 16) & 0xFF;
+    if (kind == OP_LOAD) {
+      tile_load<LPT>(tw, src, x);
+    } else if (kind != OP_KEEP) {
+      uint32_t y[LPT];
+      if (kind == OP_MUL) {
+        tile_load<LPT>(tw, src, y);
+      } else {
+#pragma unroll
+        for (int k = 0; k < LPT; k++) y[k] = x[k];
+      }
+      mt.mul(x, x, y);
+    }
+    if (dst != OP_NODST) tile_store<LPT>(tw, dst, x);
+  }
+}
+
+struct EncArgs {
+  ModDev mod;                // n^2
+  const uint32_t* nR;        // n * R mod n^2 : mul(m, nR) = m*n
+  const uint32_t* prog;      // exponent n
+  int nprog;
+  uint32_t* tbl;             // per-warp scratch tiles
+  long tbl_stride;           // words per warp
+  const uint32_t* m;         // mode 0: plaintext residues (wn words each)
+  const uint32_t* c;         // mode 1: ciphertexts to re-randomise (wc words each)
+  const uint32_t* r;         // obfuscation factors (wn words each)
+  uint32_t* out;             // wc words each
+  long count;
+  int wn, wc;
+  int mode;
+};
+
+template <int LPT, int TPI>
+__global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_encrypt(EncArgs A) {
+  using M = Mont<LPT, TPI>;
+  constexpr int IPW = 32 / TPI;
+  extern __shared__ uint32_t smem[];
+  M mt;
+  mt.init(A.mod.n, A.mod.np);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane / TPI;
+  uint32_t* sm = smem + (warp * IPW + g) * (M::L + 2);
+  const long wg = (long)blockIdx.x * (blockDim.x >> 5) + warp, nw = (long)gridDim.x * (blockDim.x >> 5);
+  uint32_t* tw = A.tbl + wg * A.tbl_stride;
+  const long ntiles = (A.count + IPW - 1) / IPW;
+  for (long tile = wg; tile < ntiles; tile += nw) {
+    long inst = tile * IPW + g;
+    bool valid = inst < A.count;
+    long ii = valid ? inst : A.count - 1;
+    uint32_t x[LPT], y[LPT];
+    mt.load_words(x, A.r + ii * A.wn, A.wn, 0);
+    mt.load_digits(y, A.mod.r2);
+    mt.mul(x, x, y);                              // Mont(r)
+    run_prog<LPT, TPI>(mt, x, A.prog, A.nprog, tw);  // Mont(r^n)
+    if (A.mode == 0) {
+      uint32_t z[LPT];
+      mt.load_words(y, A.m + ii * A.wn, A.wn, 0);
+      mt.load_digits(z, A.nR);
+      mt.mul(y, y, z);                            // m*n (plain)
+      y[0] += mt.m0 & 1u;                         // 1 + m*n
+    } else {
+      mt.load_words(y, A.c + ii * A.wc, A.wc, 0);
+    }
+    mt.mul(x, x, y);                              // plain product
+    mt.canonical(x);
+    mt.store_words(A.out + ii * A.wc, A.wc, x, sm, valid);
+  }
+}
+
+struct MulArgs {
+  ModDev mod;
+  const uint32_t* nR;
+  const uint32_t* a;
+  const uint32_t* b;      // ciphertexts (lift == 0) or plaintext residues (lift == 1)
+  uint32_t* out;
+  long count;
+  int wn, wc;
+  int lift;
+  int b_broadcast;
+};
+
+template <int LPT, int TPI>
+__global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_mulmod(MulArgs A) {
+  using M = Mont<LPT, TPI>;
+  constexpr int IPW = 32 / TPI;
+  extern __shared__ uint32_t smem[];
+  M mt;
+  mt.init(A.mod.n, A.mod.np);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane / TPI;
+  uint32_t* sm = smem + (warp * IPW + g) * (M::L + 2);
+  const long wg = (long)blockIdx.x * (blockDim.x >> 5) + warp, nw = (long)gridDim.x * (blockDim.x >> 5);
+  const long ntiles = (A.count + IPW - 1) / IPW;
+  for (long tile = wg; tile < ntiles; tile += nw) {
+    long inst = tile * IPW + g;
+    bool valid = inst < A.count;
+    long ii = valid ? inst : A.count - 1;
+    long ib = A.b_broadcast ? 0 : ii;
+    uint32_t x[LPT], y[LPT];
+    if (A.lift) {
+      mt.load_words(x, A.b + ib * A.wn, A.wn, 0);
+      mt.load_digits(y, A.nR);
+      mt.mul(y, x, y);
+      y[0] += mt.m0 & 1u;
+      mt.load_digits(x, A.mod.r2);
+      mt.mul(y, y, x);                            // Mont(1 + m n)
+    } else {
+      mt.load_words(x, A.b + ib * A.wc, A.wc, 0);
+      mt.load_digits(y, A.mod.r2);
+      mt.mul(y, x, y);                            // Mont(b)
+    }
+    mt.load_words(x, A.a + ii * A.wc, A.wc, 0);
+    mt.mul(x, x, y);                              // a*b plain
+    mt.canonical(x);
+    mt.store_words(A.out + ii * A.wc, A.wc, x, sm, valid);
+  }
+}
+
+struct HalfDev {
+  ModDev s2;                 // modulus s^2
+  ModDev s1;                 // modulus s, zero-padded to the same digit count
+  const uint32_t* hiR2;      // 2^H * R^2 mod s^2 : Montgomery form of the high half of c
+  const uint32_t* hsR;       // hs * R mod s      : mul(t, hsR) = t*hs mod s
+  const uint32_t* prog;      // exponent s - 1
+  int nprog;
+};
+
+struct DecArgs {
+  HalfDev half[2];           // [0] = p, [1] = q
+  const uint32_t* qinvR;     // q^-1 * R mod p
+  ModDev modn;               // modulus n (padded)
+  const uint32_t* qR;        // q * R mod n
+  uint32_t* tbl;
+  long tbl_stride;
+  int stash_slot;            // table slot used to park mp while the q half runs
+  const uint32_t* c;
+  uint32_t* out;
+  long count;
+  int wn, wc;
+};
+
+template <int LPT, int TPI>
+__global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_decrypt(DecArgs A) {
+  using M = Mont<LPT, TPI>;
+  constexpr int IPW = 32 / TPI;
+  extern __shared__ uint32_t smem[];
+  M mt;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane / TPI;
+  uint32_t* sm = smem + (warp * IPW + g) * (M::L + 2);
+  const long wg = (long)blockIdx.x * (blockDim.x >> 5) + warp, nw = (long)gridDim.x * (blockDim.x >> 5);
+  uint32_t* tw = A.tbl + wg * A.tbl_stride;
+  const long ntiles = (A.count + IPW - 1) / IPW;
+  const int wlo = A.wc / 2, whi = A.wc - wlo;
+  for (long tile = wg; tile < ntiles; tile += nw) {
+    long inst = tile * IPW + g;
+    bool valid = inst < A.count;
+    long ii = valid ? inst : A.count - 1;
+    const uint32_t* cw = A.c + ii * A.wc;
+    uint32_t x[LPT], y[LPT], z[LPT];
+#pragma unroll 1
+    for (int h = 0; h < 2; h++) {
+      const HalfDev& H = A.half[h];
+      mt.init(H.s2.n, H.s2.np);
+      // c mod s^2 in Montgomery form, from the two word halves of c
+      mt.load_words(x, cw, wlo, 0);
+      mt.load_digits(y, H.s2.r2);
+      mt.mul(x, x, y);
+      mt.load_words(y, cw + wlo, whi, 0);
+      mt.load_digits(z, H.hiR2);
+      mt.mul(y, y, z);
+#pragma unroll
+      for (int k = 0; k < LPT; k++) x[k] += y[k];
+      mt.renorm(x);
+      run_prog<LPT, TPI>(mt, x, H.prog, H.nprog, tw);   // Mont(c^(s-1) mod s^2)
+      mt.set_one(z);
+      mt.mul(x, x, z);
+      mt.canonical(x);                              // u = c^(s-1) mod s^2
+      // u == 0 happens only when s divides c (never for a real ciphertext); the reference's floor
+      // division (0 - 1) // s is then -1, i.e. t = s - 1 (mod s).
+      const bool uzero = mt.is_zero(x);
+      mt.decrement(x);                              // u - 1 = s * t
+      mt.init(H.s1.n, H.s1.np);
+      mt.mul_quot(x, y, x, z);                      // y <- quotient digits of (u-1)*1 w.r.t. s
+      mt.negate(y);                                 // t = (u - 1) / s
+      if (uzero) {
+#pragma unroll
+        for (int k = 0; k < LPT; k++) y[k] = mt.n[k];
+        y[0] -= mt.m0 & 1u;
+      }
+      mt.load_digits(z, H.hsR);
+      mt.mul(x, y, z);
+      mt.canonical(x);                              // ms = t * hs mod s
+      if (h == 0) tile_store<LPT>(tw, A.stash_slot, x);
+    }
+    // x = mq.  CRT recombination: m = mq + q * ((mp - mq) * q_inv mod p)   (operators.py:56)
+    mt.init(A.half[0].s1.n, A.half[0].s1.np);       // modulus p
+    mt.load_digits(y, A.half[0].s1.r1);
+    mt.mul(y, x, y);
+    mt.canonical(y);                                // mq mod p
+    tile_load<LPT>(tw, A.stash_slot, z);            // mp
+#pragma unroll
+    for (int k = 0; k < LPT; k++) y[k] = mt.n[k] + (DMASK - y[k]);
+    y[0] += mt.m0 & 1u;
+    mt.normalize(y);                                // p - (mq mod p); the carry out (= R) is dropped
+#pragma unroll
+    for (int k = 0; k < LPT; k++) y[k] += z[k];
+    mt.normalize(y);                                // mp + p - (mq mod p)  in (0, 2p)
+    mt.load_digits(z, A.qinvR);
+    mt.mul(y, y, z);
+    mt.canonical(y);                                // h in [0, p)
+    mt.init(A.modn.n, A.modn.np);
+    mt.load_digits(z, A.qR);
+    mt.mul(y, y, z);
+    mt.canonical(y);                                // q * h  (< n, exact)
+#pragma unroll
+    for (int k = 0; k < LPT; k++) x[k] += y[k];
+    mt.canonical(x);
+    mt.store_words(A.out + ii * A.wn, A.wn, x, sm, valid);
+  }
+}
+
+}  // namespace hb

@@ -94,6 +94,21 @@ struct Mont {
   // a and b may alias r.  Digits of a, b must be < 2^29 + 2^8.
   __device__ __forceinline__ void mul(uint32_t (&r)[LPT], const uint32_t (&a)[LPT],
                                       const uint32_t (&b)[LPT]) const {
+    uint32_t unused[LPT];
+    mul_impl<false>(r, a, b, unused);
+  }
+
+  // Same as mul(), and additionally hands back the Montgomery quotient digits: lane t receives
+  // digits [t*LPT, (t+1)*LPT) of Q = -(a*b) * n^-1 mod R (exact digits).  Used for exact division:
+  // when a*b is a multiple of n, a*b / n = (R - Q) mod R.
+  __device__ __forceinline__ void mul_quot(uint32_t (&r)[LPT], uint32_t (&qd)[LPT],
+                                           const uint32_t (&a)[LPT], const uint32_t (&b)[LPT]) const {
+    mul_impl<true>(r, a, b, qd);
+  }
+
+  template <bool COLLECT>
+  __device__ __forceinline__ void mul_impl(uint32_t (&r)[LPT], const uint32_t (&a)[LPT],
+                                           const uint32_t (&b)[LPT], uint32_t (&qd)[LPT]) const {
     uint64_t acc[LPT];
 #pragma unroll
     for (int i = 0; i < LPT; i++) acc[i] = 0;
@@ -106,6 +121,7 @@ struct Mont {
         acc[0] = mad_wide(a[0], bj, acc[0]);
         uint32_t q = (lo32(acc[0]) * np) & DMASK;
         q = __shfl_sync(FULLMASK, q, 0, TPI);
+        if (COLLECT) { if (s == t) qd[i] = q; }
 #pragma unroll
         for (int k = 1; k < LPT; k++) acc[k] = mad_wide(a[k], bj, acc[k]);
 #pragma unroll
@@ -212,8 +228,9 @@ struct Mont {
   }
 
   // Exact digits -> little-endian 32-bit words, staged through sm (L + 2 words owned by the group).
+  // Must be called by every lane of the warp; only groups with valid == true write to w.
   __device__ __forceinline__ void store_words(uint32_t* __restrict__ w, int nwords,
-                                              const uint32_t (&r)[LPT], uint32_t* sm) const {
+                                              const uint32_t (&r)[LPT], uint32_t* sm, bool valid = true) const {
     __syncwarp();
 #pragma unroll
     for (int i = 0; i < LPT; i++) sm[t * LPT + i] = r[i];
@@ -227,9 +244,40 @@ struct Mont {
         uint64_t v = (uint64_t)sm[D] | ((uint64_t)sm[D + 1] << RB) | ((uint64_t)sm[D + 2] << (2 * RB));
         word = (uint32_t)(v >> o);
       }
-      w[k] = word;
+      if (valid) w[k] = word;
     }
     __syncwarp();
+  }
+
+  // r = (R - r) mod R for exact digits r (two's complement in radix 2^29); result has exact digits.
+  __device__ __forceinline__ void negate(uint32_t (&r)[LPT]) const {
+#pragma unroll
+    for (int i = 0; i < LPT; i++) r[i] = DMASK - r[i];
+    r[0] += m0 & 1u;
+    normalize(r);
+  }
+
+  // r = r - 1 (mod R) for exact digits r.
+  __device__ __forceinline__ void decrement(uint32_t (&r)[LPT]) const {
+#pragma unroll
+    for (int i = 0; i < LPT; i++) r[i] += DMASK;
+    normalize(r);
+  }
+
+  // True (on every lane of the group) when all digits of the group's number are zero.
+  __device__ __forceinline__ bool is_zero(const uint32_t (&r)[LPT]) const {
+    uint32_t any = r[0];
+#pragma unroll
+    for (int i = 1; i < LPT; i++) any |= r[i];
+    uint32_t nz = (__ballot_sync(FULLMASK, any != 0) >> gshift) & GM;
+    return nz == 0;
+  }
+
+  // The integer 1 as digits.
+  __device__ __forceinline__ void set_one(uint32_t (&r)[LPT]) const {
+#pragma unroll
+    for (int i = 0; i < LPT; i++) r[i] = 0;
+    r[0] = m0 & 1u;
   }
 
   // Plain digit arrays (already radix 2^29, e.g. constants or scratch written by store_digits).
