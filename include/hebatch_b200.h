@@ -72,6 +72,31 @@ int hb_mulmod(hb_ctx* ctx, const uint32_t* a, const uint32_t* b, uint32_t* out, 
 int hb_lift_mulmod(hb_ctx* ctx, const uint32_t* a, const uint32_t* m, uint32_t* out, int64_t count,
                    int m_broadcast, void* stream);
 
+/* _pow_scalar / _k_mul, operators.py:59-67: out[i] = pow_scalar(c[i], k[i % k_period]) where residues
+ * k > n - n/3 are negative: the base becomes c^-1 mod n^2 and the exponent n - k.  k_period = 1
+ * broadcasts one scalar, = columns broadcasts a row vector over a 2-D batch, = count is element-wise.
+ * Returns HB_ERR_NOTUNIT if a needed inverse does not exist.  Synchronises `stream` internally. */
+#define HB_POW_RAW_EXPONENT 1   /* flags: exponent is the residue itself (paillier.hmul_raw, :221-228) */
+int hb_powscalar(hb_ctx* ctx, const uint32_t* c, const uint32_t* k, uint32_t* out, int64_t count,
+                 int64_t k_period, int flags, void* stream);
+/* _k_product, operators.py:75-83: out[g] = prod_{t < glen} c[g*gstride + t*estride] mod n^2.
+ * axis=None: (1, count, 0, 1); axis=0 of rows x cols: (cols, rows, 1, cols); axis=1: (rows, cols, cols, 1). */
+int hb_product(hb_ctx* ctx, const uint32_t* c, uint32_t* out, int64_t ngroups, int64_t glen,
+               int64_t gstride, int64_t estride, void* stream);
+/* _k_dot / batch_matmul, operators.py:86-94,294-317: c is rows x inner ciphertexts, k is inner x d
+ * plaintext residues (row-major), out is rows x d:  out[i][j] = prod_t pow_scalar(c[i][t], k[t][j]).
+ * Scalars whose magnitude fits 64 bits take the bucket (Pippenger) path; wider ones a generic path. */
+int hb_matvec(hb_ctx* ctx, const uint32_t* c, const uint32_t* k, uint32_t* out, int64_t rows,
+              int64_t inner, int64_t d, void* stream);
+
+/* ---- fixed-point codec (encoding.py:54-101), shared exponent per call ------------------------------
+ * *first_bad is a DEVICE int64 the caller initialises to -1; it receives the smallest element index that
+ * overflowed (encode: |mantissa| >= n/3; decode: residue inside the overflow band), or stays -1. */
+int hb_encode_f64(hb_ctx* ctx, const double* values, int exponent, uint32_t* m_out, int64_t count,
+                  int64_t* first_bad, void* stream);
+int hb_decode_f64(hb_ctx* ctx, const uint32_t* m, int exponent, double* values_out, int64_t count,
+                  int64_t* first_bad, void* stream);
+
 /* ---- host-buffer convenience path (pinned staging, side streams) --------------------------------*/
 int hb_encrypt_host(hb_ctx* ctx, const uint32_t* m, const uint32_t* r, uint32_t* out, int64_t count);
 int hb_decrypt_host(hb_ctx* ctx, const uint32_t* c, uint32_t* m_out, int64_t count);

@@ -1,121 +1,17 @@
-// C ABI of the B200 homomorphic-operator library (include/hebatch_b200.h).
-#include <cstdio>
-#include <cstring>
-#include <atomic>
-#include <mutex>
-#include <string>
-#include <vector>
-#include <cuda_runtime.h>
-
-#include "../../include/hebatch_b200.h"
-#include "hb_host.h"
+// C ABI of the B200 homomorphic-operator library (include/hebatch_b200.h): key contexts and the
+// encrypt / obfuscate / decrypt / mulmod entry points.
+#include "hb_ctx.h"
 #include "hb_kernels.cuh"
 
 using hbh::Big;
+using namespace hbi;
 
-namespace {
-
+namespace hbi {
 thread_local std::string g_err;
 std::atomic<long long> g_launches{0};
-
-int fail(int code, const std::string& msg) { g_err = msg; return code; }
-#define CU(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) \
-  return fail(HB_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); } while (0)
-
-// Instantiated limb configurations, ordered by digit count L = LPT * TPI (capacity 29*L bits).
-struct Cfg { int lpt, tpi; };
-const Cfg kCfgs[] = {{9, 4}, {18, 4}, {27, 4}, {18, 8}, {27, 8}};
-constexpr int kNumCfg = 5;
-constexpr int kMargin = 6;   // R must exceed the modulus by this many bits
-
-int pick_cfg(int bits) {
-  for (int i = 0; i < kNumCfg; i++)
-    if (29 * kCfgs[i].lpt * kCfgs[i].tpi >= bits + kMargin) return i;
-  return -1;
 }
-int window_for(int ebits) { return ebits >= 768 ? 5 : ebits >= 160 ? 4 : ebits >= 24 ? 3 : 2; }
-
-// Builder of the per-context constant block (one device allocation).
-struct ConstBlock {
-  std::vector<uint32_t> host;
-  size_t add(const std::vector<uint32_t>& v) {
-    size_t off = host.size();
-    host.insert(host.end(), v.begin(), v.end());
-    while (host.size() % 4) host.push_back(0);
-    return off;
-  }
-};
-
-struct ModOff { size_t n, r1, r2; uint32_t np; };
-
-ModOff add_modulus(ConstBlock& cb, const Big& mod, int L) {
-  ModOff m;
-  Big one{1};
-  m.n = cb.add(hbh::to_digits(mod, L));
-  m.r1 = cb.add(hbh::to_digits(hbh::shl_mod(one, 29L * L, mod), L));
-  m.r2 = cb.add(hbh::to_digits(hbh::shl_mod(one, 2 * 29L * L, mod), L));
-  m.np = hbh::neg_inv29(mod[0]);
-  return m;
-}
-
-}  // namespace
-
-struct hb_ctx {
-  int device = 0;
-  int sms = 0;
-  int key_bits = 0, wn = 0, wc = 0;
-  Big n, n2;
-  // public part
-  int cfg_pub = -1;
-  uint32_t* d_pub = nullptr;
-  ModOff mod_n2;
-  size_t off_nR = 0, off_prog_n = 0;
-  int nprog_n = 0, slots_n = 0;
-  // private part
-  bool has_private = false;
-  int cfg_priv = -1;
-  uint32_t* d_priv = nullptr;
-  struct Half { ModOff s2, s1; size_t hiR2, hsR, prog; int nprog; } half[2];
-  size_t off_qinvR = 0, off_qR = 0;
-  ModOff mod_n_priv;
-  int slots_priv = 0;
-  // host-path staging
-  std::mutex mu;
-};
 
 namespace {
-
-hb::ModDev dev_mod(const uint32_t* base, const ModOff& m) {
-  return hb::ModDev{base + m.n, base + m.r1, base + m.r2, m.np};
-}
-
-struct Launch { int blocks; int threads; size_t smem; long nwarps; };
-Launch plan(const hb_ctx* ctx, int cfg, long count) {
-  const int tpi = kCfgs[cfg].tpi, lpt = kCfgs[cfg].lpt;
-  const int ipw = 32 / tpi;
-  long ntiles = (count + ipw - 1) / ipw;
-  long blocks = (ntiles + 3) / 4;
-  long maxb = (long)ctx->sms * hb::blocks_per_sm(lpt);
-  if (blocks > maxb) blocks = maxb;
-  if (blocks < 1) blocks = 1;
-  Launch l;
-  l.blocks = (int)blocks;
-  l.threads = 128;
-  l.smem = (size_t)4 * ipw * (lpt * tpi + 2) * sizeof(uint32_t);
-  l.nwarps = blocks * 4;
-  return l;
-}
-
-#define HB_DISPATCH(cfg, KERNEL, launch, stream, args)                                           \
-  switch (cfg) {                                                                                 \
-    case 0: hb::KERNEL<9, 4><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break;  \
-    case 1: hb::KERNEL<18, 4><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break; \
-    case 2: hb::KERNEL<27, 4><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break; \
-    case 3: hb::KERNEL<18, 8><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break; \
-    case 4: hb::KERNEL<27, 8><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break; \
-    default: return fail(HB_ERR_UNSUPPORTED, "no limb configuration");                            \
-  }                                                                                              \
-  g_launches++;
 
 int encrypt_common(hb_ctx* ctx, const uint32_t* m, const uint32_t* c, const uint32_t* r, uint32_t* out,
                    int64_t count, int mode, void* stream_) {
@@ -199,6 +95,32 @@ int hb_ctx_create(hb_ctx** out, const uint32_t* n_words, int n_nwords, int devic
   std::vector<uint32_t> prog = hbh::build_program(n, window_for(ctx->key_bits), &ctx->slots_n);
   ctx->nprog_n = (int)prog.size();
   ctx->off_prog_n = cb.add(prog);
+  {
+    std::vector<uint32_t> nw(n.begin(), n.end());
+    nw.resize(ctx->wn, 0);
+    ctx->off_nwords = cb.add(nw);
+    // neg_band = n - n / 3  (operators.py:250); n / 3 by schoolbook short division
+    Big third(n.size(), 0);
+    uint64_t rem = 0;
+    for (int i = (int)n.size() - 1; i >= 0; i--) {
+      uint64_t cur = (rem << 32) | n[i];
+      third[i] = (uint32_t)(cur / 3);
+      rem = cur % 3;
+    }
+    {
+      Big mi = third;
+      mi.resize(ctx->wn, 0);
+      ctx->off_maxint = cb.add(mi);
+    }
+    Big nb = n;
+    hbh::sub_in(nb, third);
+    nb.resize(ctx->wn, 0);
+    ctx->off_negband = cb.add(nb);
+    const int T = 32 * ((29 * L + 31) / 32 / 32 + 1);
+    std::vector<uint32_t> n2w(ctx->n2.begin(), ctx->n2.end());
+    n2w.resize(T, 0);
+    ctx->off_n2words = cb.add(n2w);
+  }
   e = cudaMalloc(&ctx->d_pub, cb.host.size() * sizeof(uint32_t));
   if (e == cudaSuccess) e = cudaMemcpy(ctx->d_pub, cb.host.data(), cb.host.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) { delete ctx; return fail(HB_ERR_CUDA, cudaGetErrorString(e)); }

@@ -1,0 +1,146 @@
+// Shared internals of the C ABI translation units (not part of the public interface).
+#pragma once
+#include <cstdio>
+#include <cstring>
+#include <atomic>
+#include <mutex>
+#include <string>
+#include <vector>
+#include <cuda_runtime.h>
+
+#include "../../include/hebatch_b200.h"
+#include "hb_host.h"
+#include "mont.cuh"
+
+namespace hb {
+struct ModDev {
+  const uint32_t* n;    // modulus digits (L)
+  const uint32_t* r1;   // R mod n
+  const uint32_t* r2;   // R^2 mod n
+  uint32_t np;          // -n^-1 mod 2^29
+};
+// Resident 128-thread blocks per SM the kernels are compiled for (register budget 128 or 168).
+__host__ __device__ constexpr int blocks_per_sm(int lpt) { return lpt > 20 ? 3 : 4; }
+template <int LPT>
+__device__ __forceinline__ void tile_store(uint32_t* tw, int e, const uint32_t (&x)[LPT]) {
+  int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 0; k < LPT; k++) tw[(e * LPT + k) * 32 + lane] = x[k];
+}
+template <int LPT>
+__device__ __forceinline__ void tile_load(const uint32_t* tw, int e, uint32_t (&x)[LPT]) {
+  int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 0; k < LPT; k++) x[k] = tw[(e * LPT + k) * 32 + lane];
+}
+
+}  // namespace hb
+
+using hbh::Big;
+
+namespace hbi {
+
+extern thread_local std::string g_err;
+extern std::atomic<long long> g_launches;
+
+inline int fail(int code, const std::string& msg) { g_err = msg; return code; }
+#define CU(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) \
+  return hbi::fail(HB_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); } while (0)
+
+// Instantiated limb configurations, ordered by digit count L = LPT * TPI (capacity 29*L bits).
+struct Cfg { int lpt, tpi; };
+static const Cfg kCfgs[] = {{9, 4}, {18, 4}, {27, 4}, {18, 8}, {27, 8}};
+constexpr int kNumCfg = 5;
+constexpr int kMargin = 6;   // R must exceed the modulus by this many bits
+
+inline int pick_cfg(int bits) {
+  for (int i = 0; i < kNumCfg; i++)
+    if (29 * kCfgs[i].lpt * kCfgs[i].tpi >= bits + kMargin) return i;
+  return -1;
+}
+inline int window_for(int ebits) { return ebits >= 768 ? 5 : ebits >= 160 ? 4 : ebits >= 24 ? 3 : 2; }
+
+// Builder of the per-context constant block (one device allocation).
+struct ConstBlock {
+  std::vector<uint32_t> host;
+  size_t add(const std::vector<uint32_t>& v) {
+    size_t off = host.size();
+    host.insert(host.end(), v.begin(), v.end());
+    while (host.size() % 4) host.push_back(0);
+    return off;
+  }
+};
+
+struct ModOff { size_t n, r1, r2; uint32_t np; };
+
+inline ModOff add_modulus(ConstBlock& cb, const Big& mod, int L) {
+  ModOff m;
+  Big one{1};
+  m.n = cb.add(hbh::to_digits(mod, L));
+  m.r1 = cb.add(hbh::to_digits(hbh::shl_mod(one, 29L * L, mod), L));
+  m.r2 = cb.add(hbh::to_digits(hbh::shl_mod(one, 2 * 29L * L, mod), L));
+  m.np = hbh::neg_inv29(mod[0]);
+  return m;
+}
+
+}  // namespace hbi
+
+struct hb_ctx {
+  int device = 0;
+  int sms = 0;
+  int key_bits = 0, wn = 0, wc = 0;
+  Big n, n2;
+  // public part
+  int cfg_pub = -1;
+  uint32_t* d_pub = nullptr;
+  hbi::ModOff mod_n2;
+  size_t off_nR = 0, off_prog_n = 0;
+  size_t off_nwords = 0, off_negband = 0, off_maxint = 0, off_n2words = 0;   // n, n - n/3 (wn words); n^2 padded for k_root_inverse
+  int nprog_n = 0, slots_n = 0;
+  // private part
+  bool has_private = false;
+  int cfg_priv = -1;
+  uint32_t* d_priv = nullptr;
+  struct Half { hbi::ModOff s2, s1; size_t hiR2, hsR, prog; int nprog; } half[2];
+  size_t off_qinvR = 0, off_qR = 0;
+  hbi::ModOff mod_n_priv;
+  int slots_priv = 0;
+  // host-path staging
+  std::mutex mu;
+};
+
+namespace hbi {
+
+inline hb::ModDev dev_mod(const uint32_t* base, const ModOff& m) {
+  return hb::ModDev{base + m.n, base + m.r1, base + m.r2, m.np};
+}
+
+struct Launch { int blocks; int threads; size_t smem; long nwarps; };
+inline Launch plan(const hb_ctx* ctx, int cfg, long count) {
+  const int tpi = kCfgs[cfg].tpi, lpt = kCfgs[cfg].lpt;
+  const int ipw = 32 / tpi;
+  long ntiles = (count + ipw - 1) / ipw;
+  long blocks = (ntiles + 3) / 4;
+  long maxb = (long)ctx->sms * hb::blocks_per_sm(lpt);
+  if (blocks > maxb) blocks = maxb;
+  if (blocks < 1) blocks = 1;
+  Launch l;
+  l.blocks = (int)blocks;
+  l.threads = 128;
+  l.smem = (size_t)4 * ipw * (lpt * tpi + 2) * sizeof(uint32_t);
+  l.nwarps = blocks * 4;
+  return l;
+}
+
+#define HB_DISPATCH(cfg, KERNEL, launch, stream, args)                                           \
+  switch (cfg) {                                                                                 \
+    case 0: hb::KERNEL<9, 4><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break;  \
+    case 1: hb::KERNEL<18, 4><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break; \
+    case 2: hb::KERNEL<27, 4><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break; \
+    case 3: hb::KERNEL<18, 8><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break; \
+    case 4: hb::KERNEL<27, 8><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break; \
+    default: return hbi::fail(HB_ERR_UNSUPPORTED, "no limb configuration");                            \
+  }                                                                                              \
+  hbi::g_launches++;
+
+}  // namespace hbi

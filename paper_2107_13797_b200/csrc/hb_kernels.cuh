@@ -12,35 +12,12 @@
 //   k_decrypt   operators.py:49-56   CRT decryption
 //   k_mulmod    operators.py:70-72   a b mod n^2 (optionally b = 1 + m n, operators.py:211)
 #pragma once
-#include "mont.cuh"
+#include "hb_ctx.h"
 
 namespace hb {
 
-struct ModDev {
-  const uint32_t* n;    // modulus digits (L)
-  const uint32_t* r1;   // R mod n
-  const uint32_t* r2;   // R^2 mod n
-  uint32_t np;          // -n^-1 mod 2^29
-};
-
 // op word of the exponent program: kind | src << 8 | dst << 16
 enum : uint32_t { OP_SQR = 0, OP_MUL = 1, OP_LOAD = 2, OP_KEEP = 3, OP_NODST = 0xFF };
-
-// Resident 128-thread blocks per SM the kernels are compiled for (register budget 128 or 168).
-__host__ __device__ constexpr int blocks_per_sm(int lpt) { return lpt > 20 ? 3 : 4; }
-
-template <int LPT>
-__device__ __forceinline__ void tile_store(uint32_t* tw, int e, const uint32_t (&x)[LPT]) {
-  int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int k = 0; k < LPT; k++) tw[(e * LPT + k) * 32 + lane] = x[k];
-}
-template <int LPT>
-__device__ __forceinline__ void tile_load(const uint32_t* tw, int e, uint32_t (&x)[LPT]) {
-  int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int k = 0; k < LPT; k++) x[k] = tw[(e * LPT + k) * 32 + lane];
-}
 
 // Replays an op program on x (Montgomery form in, Montgomery form out).  Single mul call site.
 template <int LPT, int TPI>

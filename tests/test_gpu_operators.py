@@ -1,0 +1,372 @@
+"""GPU parity: every operator of paper_2107_13797_b200.operators against the CPU oracle, bit for bit.
+
+Mirrors the reference's tests/test_operators.py (golden 683, round trips, commutation, negative scalars,
+reduction-order independence, matmul == mul + sum, seed determinism, decrypt renormalisation) with the
+oracle in the role of the naive backend.
+"""
+import random
+
+import pytest
+
+import hebatch_oracle as ho
+from paper_2107_13797_b200 import operators as ops
+from paper_2107_13797_b200 import paillier
+from paper_2107_13797_b200.backends import CudaBackend
+from paper_2107_13797_b200.batches import (CiphertextBatch, ExponentMismatch, PlaintextBatch, ShapeMismatch,
+                                           encode_batch)
+
+pytestmark = pytest.mark.gpu
+
+KEYS = ["tiny", "k128", "k512", "k1024", "k2048", "k3072"]
+COUNT = {"tiny": 12, "k128": 37, "k512": 21, "k1024": 13, "k2048": 9, "k3072": 5}
+
+
+class SequenceRng(random.Random):
+    """Feeds fixed obfuscation factors (the reference's test double, tests/test_operators.py:30-37)."""
+
+    def __init__(self, seq):
+        super().__init__(0)
+        self._seq = list(seq)
+
+    def randrange(self, a, b=None, step=1):
+        return self._seq.pop(0)
+
+
+def product_keys(ok):
+    kp = paillier.keypair_from_primes(ok.p, ok.q)
+    return kp.public, kp.private
+
+
+def rand_plain(ok, pk, count, rng, shape=None, exponent=-8):
+    ms = [rng.randrange(ok.n) for _ in range(count)]
+    return PlaintextBatch(pk, shape or (count,), (exponent,), ms, True), ms
+
+
+def encrypt_oracle(ok, ms, seed):
+    rng = random.Random(seed)
+    rs = [ho.draw_unit(ok.n, rng) for _ in ms]
+    return ho.k_encrypt(ok, list(zip(ms, rs)))
+
+
+def test_golden_683(okeys):
+    ok = okeys("tiny")
+    pk, sk = product_keys(ok)
+    plain = PlaintextBatch(pk, (1,), (0,), (3,), True)
+    out = ops.batch_encrypt(pk, plain, SequenceRng([2]))
+    assert out.payload == (683,)                      # tests/test_operators.py:63-70
+    assert out.obfuscated is True
+    assert ops.batch_decrypt(sk, out).mantissas == (3,)
+    assert paillier.encrypt_raw(pk, 3, 2).value == 683    # tests/test_paillier.py:79-84
+    assert paillier.encrypt_raw(pk, 0, 1).value == 1
+    assert paillier.decrypt_raw(sk, paillier.RawCiphertext(683)) == 3
+    assert paillier.decrypt_raw(sk, paillier.RawCiphertext(1)) == 0
+
+
+def test_tiny_key_exhaustive(okeys):
+    """Every plaintext and every unit r of n = 35 (tests/test_paillier.py:152-167)."""
+    ok = okeys("tiny")
+    pk, sk = product_keys(ok)
+    units = [r for r in range(1, 35) if r % 5 and r % 7]
+    ms = [m for m in range(35) for _ in units]
+    rs = [r for _ in range(35) for r in units]
+    got = ops.raw_encrypt(pk, ms, rs)
+    assert got == ho.k_encrypt(ok, list(zip(ms, rs)))
+    assert ops.raw_decrypt(sk, got) == ms
+    # all of Z_{n^2}, units or not, through the CRT decryption
+    allc = list(range(35 * 35))
+    assert ops.raw_decrypt(sk, allc) == ho.k_decrypt(ok, allc)
+
+
+@pytest.mark.parametrize("name", KEYS)
+def test_encrypt_decrypt_obfuscate(okeys, name):
+    ok = okeys(name)
+    pk, sk = product_keys(ok)
+    rng = random.Random(5)
+    count = COUNT[name]
+    plain, ms = rand_plain(ok, pk, count, rng)
+    ms[0] = 0
+    ms[-1] = ok.n - 1
+    plain = PlaintextBatch(pk, (count,), (-8,), ms, True)
+    enc = ops.batch_encrypt(pk, plain, random.Random(77))
+    want = encrypt_oracle(ok, ms, 77)
+    assert list(enc.payload) == want
+    assert enc.shape == (count,) and enc.exponents == (-8,) and enc.obfuscated
+    dec = ops.batch_decrypt(sk, enc)
+    assert list(dec.mantissas) == ms
+    assert list(dec.mantissas) == ho.k_decrypt(ok, want)
+    assert [ho.decrypt_textbook(ok, c) for c in want[:4]] == ms[:4]
+    ob = ops.batch_obfuscate(pk, enc, random.Random(78))
+    rng2 = random.Random(78)
+    rs = [ho.draw_unit(ok.n, rng2) for _ in ms]
+    assert list(ob.payload) == ho.k_obfuscate(ok, list(zip(want, rs)))
+    assert list(ops.batch_decrypt(sk, ob).mantissas) == ms
+    # same seed, same bits (tests/test_operators.py:299-307)
+    assert ops.batch_encrypt(pk, plain, random.Random(77)) == enc
+
+
+@pytest.mark.parametrize("name", KEYS)
+def test_add(okeys, name):
+    ok = okeys(name)
+    pk, sk = product_keys(ok)
+    rng = random.Random(6)
+    count = COUNT[name]
+    pa, ma = rand_plain(ok, pk, count, rng)
+    pb, mb = rand_plain(ok, pk, count, rng)
+    ca = ops.batch_encrypt(pk, pa, random.Random(1))
+    cb = ops.batch_encrypt(pk, pb, random.Random(2))
+    s = ops.batch_add(pk, ca, cb)
+    assert list(s.payload) == ho.k_add(ok, list(zip(ca.payload, cb.payload)))
+    assert ops.batch_add(pk, cb, ca).payload == s.payload          # commutes bit-exactly
+    assert list(ops.batch_decrypt(sk, s).mantissas) == [(x + y) % ok.n for x, y in zip(ma, mb)]
+    # plaintext operand: lifted (1 + m n), flag copied from a (operators.py:209-214)
+    unob = CiphertextBatch(pk, ca.shape, ca.exponents, ca.payload, True, obfuscated=False)
+    sp = ops.batch_add(pk, unob, pb)
+    assert list(sp.payload) == ho.k_add(ok, [(c, ho.lift(ok, m)) for c, m in zip(ca.payload, mb)])
+    assert sp.obfuscated is False
+    # scalar plaintext broadcast
+    one = PlaintextBatch(pk, (1,), (-8,), (mb[0],), True)
+    sb = ops.batch_add(pk, ca, one)
+    assert list(sb.payload) == ho.k_add(ok, [(c, ho.lift(ok, mb[0])) for c in ca.payload])
+    with pytest.raises(ExponentMismatch):
+        ops.batch_add(pk, ca, CiphertextBatch(pk, cb.shape, (-9,), cb.payload, True))
+    with pytest.raises(ShapeMismatch):
+        ops.batch_add(pk, ca, CiphertextBatch(pk, (count, 1), cb.exponents, cb.payload, True))
+
+
+def small_scalars(ok, count, rng, bits=40):
+    """Residues of signed magnitudes, about half negative (n - |k|)."""
+    out = []
+    for i in range(count):
+        mag = rng.getrandbits(min(bits, ok.max_int.bit_length() - 1))
+        out.append(mag if i % 2 == 0 else (ok.n - mag) % ok.n)
+    return out
+
+
+@pytest.mark.parametrize("name", KEYS)
+def test_mul_plain(okeys, name):
+    ok = okeys(name)
+    pk, sk = product_keys(ok)
+    rng = random.Random(8)
+    rows, cols = 3, max(2, COUNT[name] // 3)
+    count = rows * cols
+    pa, ma = rand_plain(ok, pk, count, rng, shape=(rows, cols))
+    ca = ops.batch_encrypt(pk, pa, random.Random(3))
+    cpay = list(ca.payload)
+    # same-shape, mixed signs
+    ks = small_scalars(ok, count, rng)
+    kb = PlaintextBatch(pk, (rows, cols), (-3,), ks, True)
+    out = ops.batch_mul_plain(pk, ca, kb)
+    assert list(out.payload) == ho.k_mul(ok, list(zip(cpay, ks)))
+    assert out.exponents == (-11,) and out.shape == (rows, cols)
+    assert list(ops.batch_decrypt(sk, out).mantissas) == [m * k % ok.n for m, k in zip(ma, ks)]
+    # scalar broadcast: positive, negative, zero, the band edge (positive branch), an overflow-band residue
+    for k in (4 % ok.n, (ok.n - 8) % ok.n, 0, ok.n - ok.max_int, ok.n // 2):
+        sc = PlaintextBatch(pk, (1,), (-1,), (k,), True)
+        out = ops.batch_mul_plain(pk, ca, sc)
+        assert list(out.payload) == ho.k_mul(ok, [(c, k) for c in cpay]), k
+    # row vector over the columns
+    kr = small_scalars(ok, cols, rng, bits=17)
+    out = ops.batch_mul_plain(pk, ca, PlaintextBatch(pk, (cols,), (0,), kr, True))
+    assert list(out.payload) == ho.k_mul(ok, [(c, kr[i % cols]) for i, c in enumerate(cpay)])
+    # full-width random residues as scalars (acceptance criterion 3 does this on n = 35)
+    kf = [rng.randrange(ok.n) for _ in range(count)]
+    out = ops.batch_mul_plain(pk, ca, PlaintextBatch(pk, (rows, cols), (0,), kf, True))
+    assert list(out.payload) == ho.k_mul(ok, list(zip(cpay, kf)))
+    with pytest.raises(ShapeMismatch):
+        ops.batch_mul_plain(pk, ca, PlaintextBatch(pk, (cols + 1,), (0,), [1] * (cols + 1), True))
+    # hmul_raw exponentiates by the residue itself
+    k = ok.n - 5
+    assert paillier.hmul_raw(pk, paillier.RawCiphertext(cpay[0]), k).value == ho.gmp.powmod(cpay[0], k, ok.n2)
+
+
+def test_mul_plain_non_unit_raises(okeys):
+    ok = okeys("k128")
+    pk, _ = product_keys(ok)
+    bad = CiphertextBatch(pk, (2,), (0,), (ok.p * 3, 5), True)
+    with pytest.raises(ZeroDivisionError):
+        ops.batch_mul_plain(pk, bad, PlaintextBatch(pk, (1,), (0,), (ok.n - 2,), True))
+
+
+@pytest.mark.parametrize("name", KEYS)
+def test_sum(okeys, name):
+    ok = okeys(name)
+    pk, sk = product_keys(ok)
+    rng = random.Random(9)
+    rows, cols = 5, max(2, COUNT[name] // 4)
+    count = rows * cols
+    pa, ma = rand_plain(ok, pk, count, rng, shape=(rows, cols))
+    ca = ops.batch_encrypt(pk, pa, random.Random(4))
+    cpay = list(ca.payload)
+    tot = ops.batch_sum(pk, ca)
+    assert tot.payload == tuple(ho.k_product(ok, [cpay])) and tot.shape == (1,)
+    s0 = ops.batch_sum(pk, ca, axis=0)
+    assert list(s0.payload) == ho.k_product(ok, [[cpay[r * cols + c] for r in range(rows)] for c in range(cols)])
+    assert s0.shape == (cols,)
+    s1 = ops.batch_sum(pk, ca, axis=1)
+    assert list(s1.payload) == ho.k_product(ok, [[cpay[r * cols + c] for c in range(cols)] for r in range(rows)])
+    assert list(ops.batch_decrypt(sk, tot).mantissas) == [sum(ma) % ok.n]
+    # order independence (tests/test_operators.py:199-205)
+    perm = list(range(count))
+    random.Random(1).shuffle(perm)
+    shuffled = CiphertextBatch(pk, (count,), ca.exponents, [cpay[i] for i in perm], True)
+    assert ops.batch_sum(pk, shuffled).payload == tot.payload
+    with pytest.raises(ShapeMismatch):
+        ops.batch_sum(pk, shuffled, axis=0)
+
+
+def test_sum_long(okeys):
+    """Multi-pass reduction (more than one chunk level) at 1024 bits, ciphertexts tiled from a pool."""
+    ok = okeys("k1024")
+    pk, _ = product_keys(ok)
+    rng = random.Random(10)
+    pool = encrypt_oracle(ok, [rng.randrange(ok.n) for _ in range(16)], 5)
+    n_el = 5000
+    pay = [pool[(i * 7) % 16] for i in range(n_el)]
+    ca = CiphertextBatch(pk, (n_el,), (0,), pay, True)
+    assert ops.batch_sum(pk, ca).payload == tuple(ho.k_product(ok, [pay]))
+    ca2 = CiphertextBatch(pk, (1250, 4), (0,), pay, True)
+    assert list(ops.batch_sum(pk, ca2, axis=0).payload) == ho.k_product(
+        ok, [[pay[r * 4 + c] for r in range(1250)] for c in range(4)])
+
+
+@pytest.mark.parametrize("name", KEYS)
+def test_matmul(okeys, name):
+    ok = okeys(name)
+    pk, sk = product_keys(ok)
+    rng = random.Random(11)
+    inner, d = max(4, COUNT[name]), 3
+    pa, ma = rand_plain(ok, pk, inner, rng, exponent=-4)
+    ca = ops.batch_encrypt(pk, pa, random.Random(6))
+    cpay = list(ca.payload)
+    ks = small_scalars(ok, inner * d, rng, bits=52)
+    x = PlaintextBatch(pk, (inner, d), (-13,), ks, True)
+    out = ops.batch_matmul(pk, ca, x)
+    rows = (tuple(cpay),)
+    cols = tuple(tuple(ks[t * d + j] for t in range(inner)) for j in range(d))
+    assert list(out.payload) == ho.k_dot(ok, rows, cols, [(0, j) for j in range(d)])
+    assert out.shape == (d,) and out.exponents == (-17,)
+    # matmul == mul then sum, bit for bit (tests/test_operators.py:236-246)
+    tiled = CiphertextBatch(pk, (inner, d), ca.exponents, [c for c in cpay for _ in range(d)], True)
+    via = ops.batch_sum(pk, ops.batch_mul_plain(pk, tiled, x), axis=0)
+    assert via.payload == out.payload
+    want = [sum(ma[t] * ks[t * d + j] for t in range(inner)) % ok.n for j in range(d)]
+    assert list(ops.batch_decrypt(sk, out).mantissas) == want
+    # 2-D left operand and full-width scalars (general path)
+    a2 = CiphertextBatch(pk, (2, inner // 2), ca.exponents, cpay[:2 * (inner // 2)], True)
+    kf = [rng.randrange(ok.n) for _ in range((inner // 2) * 2)]
+    x2 = PlaintextBatch(pk, (inner // 2, 2), (0,), kf, True)
+    out2 = ops.batch_matmul(pk, a2, x2)
+    rows2 = tuple(tuple(cpay[i * (inner // 2) + t] for t in range(inner // 2)) for i in range(2))
+    cols2 = tuple(tuple(kf[t * 2 + j] for t in range(inner // 2)) for j in range(2))
+    assert list(out2.payload) == ho.k_dot(ok, rows2, cols2, [(i, j) for i in range(2) for j in range(2)])
+    assert out2.shape == (2, 2)
+
+
+def test_matmul_wide(okeys):
+    """Bucket path with several segments, windows and both signs: 700 x 5 at 512 bits."""
+    ok = okeys("k512")
+    pk, _ = product_keys(ok)
+    rng = random.Random(12)
+    pool = encrypt_oracle(ok, [rng.randrange(ok.n) for _ in range(32)], 7)
+    inner, d = 700, 5
+    cpay = [pool[rng.randrange(32)] for _ in range(inner)]
+    ca = CiphertextBatch(pk, (inner,), (0,), cpay, True)
+    ks = small_scalars(ok, inner * d, rng, bits=61)
+    ks[3] = 0
+    x = PlaintextBatch(pk, (inner, d), (0,), ks, True)
+    out = ops.batch_matmul(pk, ca, x)
+    cols = tuple(tuple(ks[t * d + j] for t in range(inner)) for j in range(d))
+    assert list(out.payload) == ho.k_dot(ok, (tuple(cpay),), cols, [(0, j) for j in range(d)])
+
+
+def test_codec(okeys):
+    ok = okeys("k1024")
+    pk, _ = product_keys(ok)
+    rng = random.Random(13)
+    vals = [rng.uniform(-100.0, 100.0) for _ in range(300)] + [0.0, -0.0, 0.5, -0.5, 1e-30, 2.0 ** 60, -3.75,
+                                                                 0.03125 * 3, 5e-324, 1.5 * 2 ** -8, 2.5 * 2 ** -8]
+    for exponent in (-8, -16, 0, 3, -40):
+        got = ops.batch_encode(pk, vals, exponent)
+        want = [ho.encode(ok, v, exponent)[0] for v in vals]
+        assert list(got.mantissas) == want, exponent
+        back = ops.batch_decode(pk, got)
+        assert back == [ho.decode(ok, m, exponent) for m in want]
+    # default exponent = min exact exponent: exact round trip (tests/test_encoding.py:83-89)
+    eb = encode_batch(pk, vals[:50])
+    assert ops.batch_decode(pk, eb) == vals[:50]
+    assert eb.exponents[0] == min(ho.exact_exponent(v) for v in vals[:50])
+    # big mantissas: correct rounding of > 53-bit magnitudes, both signs
+    big = [rng.randrange(ok.max_int) for _ in range(64)] + [ok.n - rng.randrange(1, ok.max_int) for _ in range(64)]
+    pb = PlaintextBatch(pk, (128,), (-200,), big, True)
+    assert ops.batch_decode(pk, pb) == [ho.decode(ok, m, -200) for m in big]
+    from paper_2107_13797_b200.encoding import FixedPointOverflow
+    with pytest.raises(FixedPointOverflow):
+        ops.batch_encode(pk, [1.0, 2.0 ** 1100 if False else 1e300], -200)
+    with pytest.raises(FixedPointOverflow):
+        ops.batch_decode(pk, PlaintextBatch(pk, (2,), (0,), (1, ok.n // 2), True))
+
+
+def test_codec_tiny_band(okeys):
+    """n = 35: max_int = 11, overflow band [11, 24] (tests/test_encoding.py:73-81)."""
+    ok = okeys("tiny")
+    pk, _ = product_keys(ok)
+    from paper_2107_13797_b200.encoding import FixedPointOverflow
+    assert list(ops.batch_encode(pk, [10.0, -10.0, 0.5], 0).mantissas) == [10, 25, 0]
+    assert list(ops.batch_encode(pk, [0.5, 1.5, 2.5, -0.5, -1.5], 0).mantissas) == [0, 2, 2, 0, 33]
+    with pytest.raises(FixedPointOverflow):
+        ops.batch_encode(pk, [11.0], 0)
+    assert ops.batch_decode(pk, PlaintextBatch(pk, (3,), (0,), (10, 25, 0), True)) == [10.0, -10.0, 0.0]
+    for m in (11, 24):
+        with pytest.raises(FixedPointOverflow):
+            ops.batch_decode(pk, PlaintextBatch(pk, (1,), (0,), (m,), True))
+
+
+def test_decrypt_renormalises(okeys):
+    """Exponents below the floor are lifted after decryption (tests/test_operators.py:310-321)."""
+    ok = okeys("k512")
+    pk, sk = product_keys(ok)
+    vals = [0.75, -1.5, 3.0]
+    plain = encode_batch(pk, vals, target_exponent=-40)
+    enc = ops.batch_encrypt(pk, plain, random.Random(1))
+    dec = ops.batch_decrypt(sk, enc)
+    want = [ho.renormalize(ok, m, -40) for m in plain.mantissas]
+    assert [(e.mantissa, e.exponent) for e in (dec.element(i) for i in range(3))] == want
+    assert ops.batch_decrypt(sk, enc, min_exponent=-64).exponents == (-40,)
+
+
+def test_backend_run_contract(okeys):
+    """Level-1 plug-in: CudaBackend.run(kernel, common, items) with the reference's common tuples."""
+    ok = okeys("k512")
+    pk, sk = product_keys(ok)
+    be = CudaBackend()
+    rng = random.Random(14)
+    ms = [rng.randrange(ok.n) for _ in range(6)]
+    rs = [ho.draw_unit(ok.n, rng) for _ in ms]
+    cs = be.run(ops._k_encrypt, (ok.n, ok.n2), list(zip(ms, rs)))
+    assert cs == ho.k_encrypt(ok, list(zip(ms, rs)))
+    assert be.run(ops._k_obfuscate, (ok.n, ok.n2), list(zip(cs, rs))) == ho.k_obfuscate(ok, list(zip(cs, rs)))
+    common = (ok.p, ok.q, ok.p2, ok.q2, ok.hp, ok.hq, ok.q_inv)
+    assert be.run(ops._k_decrypt, common, cs) == ms
+    ks = small_scalars(ok, 6, rng)
+    assert be.run(ops._k_mul, (ok.n, ok.n2, ok.neg_band), list(zip(cs, ks))) == ho.k_mul(ok, list(zip(cs, ks)))
+    assert be.run(ops._k_add, ok.n2, list(zip(cs, cs[::-1]))) == ho.k_add(ok, list(zip(cs, cs[::-1])))
+    groups = [tuple(cs[:3]), tuple(cs[3:]), ()]
+    assert be.run(ops._k_product, ok.n2, groups) == ho.k_product(ok, groups)
+    rows = (tuple(cs[:3]), tuple(cs[3:]))
+    cols = (tuple(ks[:3]), tuple(ks[3:]))
+    items = [(0, 0), (1, 1), (0, 1)]
+    assert be.run(ops._k_dot, (ok.n, ok.n2, ok.neg_band, rows, cols), items) == ho.k_dot(ok, rows, cols, items)
+    assert be.run(ops._k_encode, (pk, -8), [1.5, -2.25]) == [ho.encode(ok, v, -8)[0] for v in (1.5, -2.25)]
+    assert be.run(ops._k_decode, (pk, -8), [384, ok.n - 576]) == [1.5, -2.25]
+    assert be.run(ops._k_add, ok.n2, []) == []
+
+
+def test_empty_batches(okeys):
+    ok = okeys("k128")
+    pk, sk = product_keys(ok)
+    empty = PlaintextBatch(pk, (0,), (0,), (), True)
+    enc = ops.batch_encrypt(pk, empty, random.Random(1))
+    assert enc.count == 0 and enc.payload == ()
+    assert ops.batch_decrypt(sk, enc).mantissas == ()
+    assert ops.batch_sum(pk, enc).payload == (1,)
+    assert ops.batch_add(pk, enc, enc).payload == ()
