@@ -1,0 +1,376 @@
+#!/usr/bin/env python
+"""Headline benchmark: batched Paillier-2048 encrypt + decrypt of 1M fixed-point values per GPU
+(BASELINE.json configs[1]), plus the encrypted matvec of configs[2] as an extra.
+
+    python bench.py --gpus N --steps K --warmup W            (N > 1: launched under torchrun, one rank per GPU)
+    python bench.py --impl reference ...                     (the reference's CPU algorithm on the host cores)
+
+A step = one pass of the hot path over one batch: encrypt `count` residues, then decrypt the resulting
+ciphertexts (2 * count Paillier operations).  `value` is timed with the inputs already resident in HBM;
+`e2e` goes through the C ABI's host-buffer entry points (pinned staging, H2D and D2H inside the timed
+region).  Every rank processes its own `count` elements (independent shards, no data-path collective):
+weak scaling.  Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import random
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+for _p in (ROOT, os.path.join(ROOT, "oracle")):
+    if _p not in sys.path:
+        sys.path.insert(0, _p)
+
+KEY_BITS = 2048
+KEY_SEED = 7
+# canonical limb products per operation at key 2048: modmul(L) = 2 L^2 + L with
+# 32-bit limbs, modexp(b) = 1.25 b modmuls
+LP_ENCRYPT = (1.25 * 2048 + 3) * (2 * 128 * 128 + 128) + 64 * 64
+LP_DECRYPT = 2 * (1.25 * 1024 + 3) * (2 * 64 * 64 + 64)
+LP_MODMUL = 2 * 128 * 128 + 128
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--count", type=int, default=1_000_000, help="elements per GPU per step")
+    ap.add_argument("--cpu-sample", type=int, default=4096, help="elements of the bounded CPU sample")
+    ap.add_argument("--no-matvec", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def bench_key():
+    """keygen(2048, default_rng(7)) -- the config-2 key."""
+    import hebatch_oracle as ho
+    return ho.keygen(KEY_BITS, random.Random(KEY_SEED))
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "250"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._pump, daemon=True).start()
+        except OSError:
+            self.proc = None
+
+    def _pump(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0])); smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        busy = [v for v in sm if v > 0.5 * max(smax or [1])] or sm
+        return {"sm_mhz": statistics.median(busy) if busy else None,
+                "sm_max_mhz": max(smax) if smax else None, "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def cpu_reference_rate(key, sample: int, rng_seed: int = 1):
+    """The reference's CPU algorithm (GMP powm, all host threads) on a bounded sample of the workload."""
+    import numpy as np
+    import cpuref
+    wn, wc = cpuref.widths(key.n)
+    rs = np.random.default_rng(rng_seed)
+    m = rs.integers(0, 2 ** 32, size=(sample, wn), dtype=np.uint32); m[:, -1] = 0
+    r = rs.integers(0, 2 ** 32, size=(sample, wn), dtype=np.uint32); r[:, -1] = 1
+    threads = cpuref.threads()
+    t0 = time.perf_counter()
+    c = cpuref.encrypt_words(key.n, m, r, threads)
+    t1 = time.perf_counter()
+    back = cpuref.decrypt_words(key, c, threads)
+    t2 = time.perf_counter()
+    if not (back == m).all():
+        raise RuntimeError("CPU reference round trip failed")
+    return {"ops_per_s": 2 * sample / (t2 - t0), "encrypt_per_s": sample / (t1 - t0),
+            "decrypt_per_s": sample / (t2 - t1), "seconds": t2 - t0, "threads": threads}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    key = bench_key()
+    sample = args.cpu_sample
+    for _ in range(args.warmup):
+        cpu_reference_rate(key, max(64, sample // 16))
+    times, last = [], None
+    for _ in range(args.steps):
+        last = cpu_reference_rate(key, sample)
+        times.append(last["seconds"])
+    total = sum(times)
+    value = 2 * sample * args.steps / total
+    line = {
+        "impl": "reference", "metric": "paillier2048_encrypt_decrypt_ops_per_s", "value": value,
+        "unit": "ops/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": "batched Paillier-2048 encrypt + decrypt (BASELINE configs[1])",
+                   "key_bits": KEY_BITS, "count_per_step": sample,
+                   "note": "bounded sample of the 1M-element workload; per-element cost is uniform"},
+        "cpu_baseline": {"value": value, "unit": "ops/s", "cores": last["threads"], "kind": "port",
+                         "sample": f"{sample} encrypt + {sample} decrypt per step, GMP mpz_powm under OpenMP "
+                                   "(oracle/cpu_ref.c), the arithmetic the reference reaches through gmpy2"},
+        "e2e": {"value": value, "unit": "ops/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def measured_imad_peak():
+    """Live integer-multiply peak (LP/s) from the standalone microbenchmark; falls back to the committed one."""
+    exe = os.path.join(ROOT, "build", "imad_peak2")
+    try:
+        out = subprocess.run([exe], capture_output=True, text=True, timeout=120, check=True).stdout
+        data = json.loads(out.strip().splitlines()[-1])
+        return data["lp_per_s_wide_carry"], "measured live (build/imad_peak2, IMAD.WIDE.U32.X chains)"
+    except Exception:
+        with open(os.path.join(ROOT, "profiles", "r01_imad_peak2.json")) as fh:
+            data = json.load(fh)
+        return data["lp_per_s_wide_carry"], "profiles/r01_imad_peak2.json (earlier run on this pool)"
+
+
+def run_b200(args):
+    import numpy as np
+    import torch
+    from paper_2107_13797_b200 import _native, device
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist_mod
+        dist = dist_mod
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    key = bench_key()
+    lib = _native.lib()
+    ctx = device.context_for(key.n)
+    ctx.set_private(key.p, key.q, key.hp, key.hq, key.q_inv)
+    wn, wc = ctx.wn, ctx.wc
+    count = args.count
+    stream = device.current_stream_ptr()
+
+    # synthetic residues: config 2 encodes uniform(-100, 100) at exponent -8 (39-bit magnitudes, half of them
+    # negative residues n - |x|): produced by the device codec, seeded per rank
+    g = torch.Generator(device="cuda"); g.manual_seed(1234 + rank)
+    vals = (torch.rand(count, generator=g, device="cuda", dtype=torch.float64) * 200.0 - 100.0)
+    m = torch.empty((count, wn), dtype=torch.int32, device="cuda")
+    bad = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    _native.check(lib.hb_encode_f64(ctx.handle, vals.data_ptr(), -8, m.data_ptr(), count, bad.data_ptr(), stream))
+    # obfuscation factors: uniform below 2^(key_bits - 32) < n (gcd with n is 1 with overwhelming probability;
+    # the reference's own draw is rejection-sampled on the host and is not part of the timed hot path)
+    r = torch.randint(-2 ** 31, 2 ** 31 - 1, (count, wn), generator=g, device="cuda", dtype=torch.int32)
+    r[:, -1] = 1
+    c = torch.empty((count, wc), dtype=torch.int32, device="cuda")
+    back = torch.empty((count, wn), dtype=torch.int32, device="cuda")
+
+    def step():
+        _native.check(lib.hb_encrypt(ctx.handle, m.data_ptr(), r.data_ptr(), c.data_ptr(), count, stream))
+        _native.check(lib.hb_decrypt(ctx.handle, c.data_ptr(), back.data_ptr(), count, stream))
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    if not torch.equal(back, m):
+        raise SystemExit("round trip failed: decrypt(encrypt(m)) != m")
+    # spot check against the CPU oracle (GMP) on a prefix
+    import cpuref
+    chk = 64
+    want = cpuref.encrypt_words(key.n, m[:chk].cpu().numpy().view(np.uint32), r[:chk].cpu().numpy().view(np.uint32))
+    if not np.array_equal(want, c[:chk].cpu().numpy().view(np.uint32)):
+        raise SystemExit("ciphertexts differ from the CPU oracle")
+
+    sampler = ClockSampler(local)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    launches0 = device.launch_count()
+    barrier()
+    sampler.start()
+    enc_ms = dec_ms = 0.0
+    t_wall0 = time.perf_counter()
+    e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e_start.record()
+    for _ in range(args.steps):
+        ev[0].record()
+        _native.check(lib.hb_encrypt(ctx.handle, m.data_ptr(), r.data_ptr(), c.data_ptr(), count, stream))
+        ev[1].record()
+        _native.check(lib.hb_decrypt(ctx.handle, c.data_ptr(), back.data_ptr(), count, stream))
+        ev[2].record()
+        ev[2].synchronize()
+        enc_ms += ev[0].elapsed_time(ev[1])
+        dec_ms += ev[1].elapsed_time(ev[2])
+    e_end.record()
+    barrier()
+    clocks = sampler.stop()
+    launches = device.launch_count() - launches0
+    elapsed_ms = e_start.elapsed_time(e_end)
+    t = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda")
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed_ms = float(t.item())
+    ms_per_step = elapsed_ms / args.steps
+    value = 2.0 * count * world / (ms_per_step * 1e-3)
+
+    # ---- end to end through the host-buffer C ABI (rank-local shard, pinned staging inside the library)
+    e2e = None
+    if not args.no_e2e:
+        hm = m.cpu().numpy().view(np.uint32)
+        hr = r.cpu().numpy().view(np.uint32)
+        hc = np.empty((count, wc), np.uint32)
+        hb = np.empty((count, wn), np.uint32)
+
+        def host_step():
+            _native.check(lib.hb_encrypt_host(ctx.handle, hm.ctypes.data, hr.ctypes.data, hc.ctypes.data, count))
+            _native.check(lib.hb_decrypt_host(ctx.handle, hc.ctypes.data, hb.ctypes.data, count))
+
+        host_step()
+        barrier()
+        e2e_steps = max(1, min(args.steps, 2))
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            host_step()
+        barrier()
+        dt = time.perf_counter() - t0
+        if not np.array_equal(hb, hm):
+            raise SystemExit("host-path round trip failed")
+        tt = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        if dist is not None:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dt = float(tt.item())
+        e2e = {"value": 2.0 * count * world * e2e_steps / dt, "unit": "ops/s",
+               "h2d_bytes_per_step": int(count * (2 * wn + wc) * 4), "d2h_bytes_per_step": int(count * (wc + wn) * 4),
+               "steps": e2e_steps, "api": "hb_encrypt_host + hb_decrypt_host (include/hebatch_b200.h)"}
+
+    # ---- extra: encrypted matvec, BASELINE configs[2] (100k x 100, sharded by rows across ranks)
+    extras = {"encrypt_per_s_per_gpu": count * args.steps / (enc_ms * 1e-3),
+              "decrypt_per_s_per_gpu": count * args.steps / (dec_ms * 1e-3)}
+    if not args.no_matvec and count >= 100_000:
+        inner, d = 100_000 // world, 100
+        xg = torch.rand(inner * d, generator=g, device="cuda", dtype=torch.float64) * 2.0 - 1.0
+        xk = torch.empty((inner * d, wn), dtype=torch.int32, device="cuda")
+        _native.check(lib.hb_encode_f64(ctx.handle, xg.data_ptr(), -13, xk.data_ptr(), inner * d, bad.data_ptr(), stream))
+        mv = torch.empty((d, wc), dtype=torch.int32, device="cuda")
+        _native.check(lib.hb_matvec(ctx.handle, c.data_ptr(), xk.data_ptr(), mv.data_ptr(), 1, inner, d, stream))
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        reps = 2
+        for _ in range(reps):
+            _native.check(lib.hb_matvec(ctx.handle, c.data_ptr(), xk.data_ptr(), mv.data_ptr(), 1, inner, d, stream))
+        b.record()
+        barrier()
+        mv_ms = a.elapsed_time(b) / reps
+        tm = torch.tensor([mv_ms], dtype=torch.float64, device="cuda")
+        if dist is not None:
+            dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        mv_ms = float(tm.item())
+        terms = 100_000 // world * world * d
+        extras["matvec_100k_x_100_ms"] = mv_ms
+        extras["matvec_terms_per_s"] = terms / (mv_ms * 1e-3)
+        # canonical work: (1.25 * 52 + 1) modmuls per term (SURVEY.md 8d, 52-bit scalars)
+        extras["matvec_canonical_lp_per_s"] = terms * (1.25 * 52 + 1) * LP_MODMUL / (mv_ms * 1e-3)
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    peak, peak_src = measured_imad_peak()
+    enc_s = enc_ms * 1e-3 / args.steps            # average k_encrypt launch duration (one launch per step)
+    achieved = LP_ENCRYPT * count / enc_s
+    roofline = {
+        "bound": "imad", "kernel": "k_encrypt<18,8>", "achieved": achieved / 1e12, "peak": peak / 1e12,
+        "unit": "TLP/s (1e12 32x32->64 limb products per second)", "frac": achieved / peak, "traffic": None,
+        "peak_source": peak_src,
+        "note": "integer-multiply bound, not HBM: algorithmic bytes per encrypt are 1 KiB against 8.4e7 limb products",
+        "hbm": {"achieved_gbs": count * (2 * wn + wc) * 4 / enc_s / 1e9, "peak_gbs": _hbm_peak()},
+        "decrypt_frac": (LP_DECRYPT * count / (dec_ms * 1e-3 / args.steps)) / peak,
+    }
+    if "matvec_canonical_lp_per_s" in extras:
+        roofline["matvec_frac_canonical"] = extras["matvec_canonical_lp_per_s"] / peak
+    cpu = cpu_reference_rate(key, args.cpu_sample)
+    line = {
+        "metric": "paillier2048_encrypt_decrypt_ops_per_s", "value": value, "unit": "ops/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": {"workload": "batched Paillier-2048 encrypt + decrypt of 1M fixed-point values per GPU "
+                               "(BASELINE configs[1])",
+                   "key_bits": KEY_BITS, "count_per_gpu": count, "parallelism": f"shard{world}",
+                   "l2": "inputs per step (1 GiB) exceed the 126 MB L2; no explicit flush"},
+        "clocks": clocks, "e2e": e2e, "gpu_launches": launches, "roofline": roofline,
+        "cpu_baseline": {"value": cpu["ops_per_s"], "unit": "ops/s", "cores": cpu["threads"], "kind": "port",
+                         "sample": f"{args.cpu_sample} encrypt + {args.cpu_sample} decrypt, GMP mpz_powm under "
+                                   f"OpenMP (oracle/cpu_ref.c); encrypt {cpu['encrypt_per_s']:.1f}/s, "
+                                   f"decrypt {cpu['decrypt_per_s']:.1f}/s"},
+        "extras": extras,
+    }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def _hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)["hbm_gbs"]
+    except Exception:
+        return 6650.0
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()
