@@ -91,7 +91,7 @@ int hb_ctx_create(hb_ctx** out, const uint32_t* n_words, int n_nwords, int devic
   const int L = kCfgs[ctx->cfg_pub].lpt * kCfgs[ctx->cfg_pub].tpi;
   ConstBlock cb;
   ctx->mod_n2 = add_modulus(cb, ctx->n2, L);
-  ctx->off_nR = cb.add(hbh::to_digits(hbh::shl_mod(n, 29L * L, ctx->n2), L));
+  ctx->off_nR = cb.add(hbh::to_limbs(hbh::shl_mod(n, 32L * L, ctx->n2), L));
   std::vector<uint32_t> prog = hbh::build_program(n, window_for(ctx->key_bits), &ctx->slots_n);
   ctx->nprog_n = (int)prog.size();
   ctx->off_prog_n = cb.add(prog);
@@ -116,7 +116,7 @@ int hb_ctx_create(hb_ctx** out, const uint32_t* n_words, int n_nwords, int devic
     hbh::sub_in(nb, third);
     nb.resize(ctx->wn, 0);
     ctx->off_negband = cb.add(nb);
-    const int T = 32 * ((29 * L + 31) / 32 / 32 + 1);
+    const int T = 32 * (L / 32 + 1);
     std::vector<uint32_t> n2w(ctx->n2.begin(), ctx->n2.end());
     n2w.resize(T, 0);
     ctx->off_n2words = cb.add(n2w);
@@ -152,8 +152,8 @@ int hb_ctx_set_private(hb_ctx* ctx, const uint32_t* p_, const uint32_t* q_, cons
   for (int h = 0; h < 2; h++) {
     ctx->half[h].s2 = add_modulus(cb, s2[h], L);
     ctx->half[h].s1 = add_modulus(cb, s[h], L);
-    ctx->half[h].hiR2 = cb.add(hbh::to_digits(hbh::shl_mod(one, 32L * wlo + 2 * 29L * L, s2[h]), L));
-    ctx->half[h].hsR = cb.add(hbh::to_digits(hbh::shl_mod(hs[h], 29L * L, s[h]), L));
+    ctx->half[h].hiR2 = cb.add(hbh::to_limbs(hbh::shl_mod(one, 32L * wlo + 2 * 32L * L, s2[h]), L));
+    ctx->half[h].hsR = cb.add(hbh::to_limbs(hbh::shl_mod(hs[h], 32L * L, s[h]), L));
     Big e = hbh::sub_small(s[h], 1);
     int used = 0;
     std::vector<uint32_t> prog = hbh::build_program(e, window_for(hbh::bitlen(e)), &used);
@@ -161,9 +161,9 @@ int hb_ctx_set_private(hb_ctx* ctx, const uint32_t* p_, const uint32_t* q_, cons
     ctx->half[h].nprog = (int)prog.size();
     ctx->half[h].prog = cb.add(prog);
   }
-  ctx->off_qinvR = cb.add(hbh::to_digits(hbh::shl_mod(qinv, 29L * L, p), L));
+  ctx->off_qinvR = cb.add(hbh::to_limbs(hbh::shl_mod(qinv, 32L * L, p), L));
   ctx->mod_n_priv = add_modulus(cb, ctx->n, L);
-  ctx->off_qR = cb.add(hbh::to_digits(hbh::shl_mod(q, 29L * L, ctx->n), L));
+  ctx->off_qR = cb.add(hbh::to_limbs(hbh::shl_mod(q, 32L * L, ctx->n), L));
   ctx->slots_priv = slots;
   if (ctx->d_priv) { cudaFree(ctx->d_priv); ctx->d_priv = nullptr; }
   CU(cudaMalloc(&ctx->d_priv, cb.host.size() * sizeof(uint32_t)));

@@ -10,14 +10,14 @@
 
 #include "../../include/hebatch_b200.h"
 #include "hb_host.h"
-#include "mont.cuh"
+#include "mont32.cuh"
 
 namespace hb {
 struct ModDev {
   const uint32_t* n;    // modulus digits (L)
   const uint32_t* r1;   // R mod n
   const uint32_t* r2;   // R^2 mod n
-  uint32_t np;          // -n^-1 mod 2^29
+  uint32_t np;          // -n^-1 mod 2^32
 };
 // Resident 128-thread blocks per SM the kernels are compiled for (register budget 128 or 168).
 __host__ __device__ constexpr int blocks_per_sm(int lpt) { return lpt > 20 ? 3 : 4; }
@@ -47,15 +47,14 @@ inline int fail(int code, const std::string& msg) { g_err = msg; return code; }
 #define CU(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) \
   return hbi::fail(HB_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); } while (0)
 
-// Instantiated limb configurations, ordered by digit count L = LPT * TPI (capacity 29*L bits).
+// Instantiated limb configurations, ordered by limb count L = LPT * TPI (capacity 32*L bits).
 struct Cfg { int lpt, tpi; };
-static const Cfg kCfgs[] = {{9, 4}, {18, 4}, {27, 4}, {18, 8}, {27, 8}};
+static const Cfg kCfgs[] = {{8, 4}, {16, 4}, {24, 4}, {16, 8}, {24, 8}};
 constexpr int kNumCfg = 5;
-constexpr int kMargin = 6;   // R must exceed the modulus by this many bits
 
 inline int pick_cfg(int bits) {
   for (int i = 0; i < kNumCfg; i++)
-    if (29 * kCfgs[i].lpt * kCfgs[i].tpi >= bits + kMargin) return i;
+    if (32 * kCfgs[i].lpt * kCfgs[i].tpi >= bits) return i;
   return -1;
 }
 inline int window_for(int ebits) { return ebits >= 768 ? 5 : ebits >= 160 ? 4 : ebits >= 24 ? 3 : 2; }
@@ -76,10 +75,10 @@ struct ModOff { size_t n, r1, r2; uint32_t np; };
 inline ModOff add_modulus(ConstBlock& cb, const Big& mod, int L) {
   ModOff m;
   Big one{1};
-  m.n = cb.add(hbh::to_digits(mod, L));
-  m.r1 = cb.add(hbh::to_digits(hbh::shl_mod(one, 29L * L, mod), L));
-  m.r2 = cb.add(hbh::to_digits(hbh::shl_mod(one, 2 * 29L * L, mod), L));
-  m.np = hbh::neg_inv29(mod[0]);
+  m.n = cb.add(hbh::to_limbs(mod, L));
+  m.r1 = cb.add(hbh::to_limbs(hbh::shl_mod(one, 32L * L, mod), L));
+  m.r2 = cb.add(hbh::to_limbs(hbh::shl_mod(one, 2 * 32L * L, mod), L));
+  m.np = hbh::neg_inv32(mod[0]);
   return m;
 }
 
@@ -127,18 +126,19 @@ inline Launch plan(const hb_ctx* ctx, int cfg, long count) {
   Launch l;
   l.blocks = (int)blocks;
   l.threads = 128;
-  l.smem = (size_t)4 * ipw * (lpt * tpi + 2) * sizeof(uint32_t);
+  l.smem = 0;
+  (void)ipw;
   l.nwarps = blocks * 4;
   return l;
 }
 
 #define HB_DISPATCH(cfg, KERNEL, launch, stream, args)                                           \
   switch (cfg) {                                                                                 \
-    case 0: hb::KERNEL<9, 4><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break;  \
-    case 1: hb::KERNEL<18, 4><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break; \
-    case 2: hb::KERNEL<27, 4><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break; \
-    case 3: hb::KERNEL<18, 8><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break; \
-    case 4: hb::KERNEL<27, 8><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break; \
+    case 0: hb::KERNEL<8, 4><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break;  \
+    case 1: hb::KERNEL<16, 4><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break; \
+    case 2: hb::KERNEL<24, 4><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break; \
+    case 3: hb::KERNEL<16, 8><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break; \
+    case 4: hb::KERNEL<24, 8><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break; \
     default: return hbi::fail(HB_ERR_UNSUPPORTED, "no limb configuration");                            \
   }                                                                                              \
   hbi::g_launches++;

@@ -66,24 +66,19 @@ inline Big shl_mod(Big x, long k, const Big& n) {
 }
 inline Big sub_small(Big a, uint32_t v) { Big b{v}; sub_in(a, b); trim(a); return a; }
 
-constexpr int RB = 29;
-constexpr uint32_t DMASK = (1u << RB) - 1u;
+constexpr int RB = 32;      // radix bits of the device representation
 
-inline std::vector<uint32_t> to_digits(const Big& a, int L) {
+// the L 32-bit limbs of a (zero padded)
+inline std::vector<uint32_t> to_limbs(const Big& a, int L) {
   std::vector<uint32_t> d(L, 0);
-  for (int i = 0; i < L; i++) {
-    long b = (long)i * RB;
-    size_t k = b >> 5; int s = b & 31;
-    uint64_t lo = k < a.size() ? a[k] : 0, hi = k + 1 < a.size() ? a[k + 1] : 0;
-    d[i] = (uint32_t)(((lo | (hi << 32)) >> s) & DMASK);
-  }
+  for (int i = 0; i < L && i < (int)a.size(); i++) d[i] = a[i];
   return d;
 }
-// -n^-1 mod 2^29 for odd n
-inline uint32_t neg_inv29(uint32_t n0) {
+// -n^-1 mod 2^32 for odd n
+inline uint32_t neg_inv32(uint32_t n0) {
   uint32_t inv = n0;                     // correct to 3 bits
   for (int i = 0; i < 5; i++) inv *= 2u - n0 * inv;
-  return (0u - inv) & DMASK;
+  return 0u - inv;
 }
 
 enum : uint32_t { OP_SQR = 0, OP_MUL = 1, OP_LOAD = 2, OP_KEEP = 3, OP_NODST = 0xFF };

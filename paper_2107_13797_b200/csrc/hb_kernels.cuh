@@ -63,11 +63,9 @@ template <int LPT, int TPI>
 __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_encrypt(EncArgs A) {
   using M = Mont<LPT, TPI>;
   constexpr int IPW = 32 / TPI;
-  extern __shared__ uint32_t smem[];
   M mt;
   mt.init(A.mod.n, A.mod.np);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane / TPI;
-  uint32_t* sm = smem + (warp * IPW + g) * (M::L + 2);
   const long wg = (long)blockIdx.x * (blockDim.x >> 5) + warp, nw = (long)gridDim.x * (blockDim.x >> 5);
   uint32_t* tw = A.tbl + wg * A.tbl_stride;
   const long ntiles = (A.count + IPW - 1) / IPW;
@@ -76,22 +74,22 @@ __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_encrypt(EncArgs A) 
     bool valid = inst < A.count;
     long ii = valid ? inst : A.count - 1;
     uint32_t x[LPT], y[LPT];
-    mt.load_words(x, A.r + ii * A.wn, A.wn, 0);
-    mt.load_digits(y, A.mod.r2);
+    mt.load_words(x, A.r + ii * A.wn, A.wn);
+    mt.load_limbs(y, A.mod.r2);
     mt.mul(x, x, y);                              // Mont(r)
     run_prog<LPT, TPI>(mt, x, A.prog, A.nprog, tw);  // Mont(r^n)
     if (A.mode == 0) {
       uint32_t z[LPT];
-      mt.load_words(y, A.m + ii * A.wn, A.wn, 0);
-      mt.load_digits(z, A.nR);
+      mt.load_words(y, A.m + ii * A.wn, A.wn);
+      mt.load_limbs(z, A.nR);
       mt.mul(y, y, z);                            // m*n (plain)
-      y[0] += mt.m0 & 1u;                         // 1 + m*n
+      mt.set_one(z);
+      mt.add_mod(y, y, z);                        // 1 + m*n  (< n^2, nothing is reduced)
     } else {
-      mt.load_words(y, A.c + ii * A.wc, A.wc, 0);
+      mt.load_words(y, A.c + ii * A.wc, A.wc);
     }
-    mt.mul(x, x, y);                              // plain product
-    mt.canonical(x);
-    mt.store_words(A.out + ii * A.wc, A.wc, x, sm, valid);
+    mt.mul(x, x, y);                              // plain product, canonical
+    mt.store_words(A.out + ii * A.wc, A.wc, x, valid);
   }
 }
 
@@ -111,11 +109,9 @@ template <int LPT, int TPI>
 __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_mulmod(MulArgs A) {
   using M = Mont<LPT, TPI>;
   constexpr int IPW = 32 / TPI;
-  extern __shared__ uint32_t smem[];
   M mt;
   mt.init(A.mod.n, A.mod.np);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane / TPI;
-  uint32_t* sm = smem + (warp * IPW + g) * (M::L + 2);
   const long wg = (long)blockIdx.x * (blockDim.x >> 5) + warp, nw = (long)gridDim.x * (blockDim.x >> 5);
   const long ntiles = (A.count + IPW - 1) / IPW;
   for (long tile = wg; tile < ntiles; tile += nw) {
@@ -125,21 +121,19 @@ __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_mulmod(MulArgs A) {
     long ib = A.b_broadcast ? 0 : ii;
     uint32_t x[LPT], y[LPT];
     if (A.lift) {
-      mt.load_words(x, A.b + ib * A.wn, A.wn, 0);
-      mt.load_digits(y, A.nR);
-      mt.mul(y, x, y);
-      y[0] += mt.m0 & 1u;
-      mt.load_digits(x, A.mod.r2);
-      mt.mul(y, y, x);                            // Mont(1 + m n)
+      mt.load_words(x, A.b + ib * A.wn, A.wn);
+      mt.load_limbs(y, A.nR);
+      mt.mul(y, x, y);                            // m*n
+      mt.set_one(x);
+      mt.add_mod(y, y, x);                        // 1 + m*n
     } else {
-      mt.load_words(x, A.b + ib * A.wc, A.wc, 0);
-      mt.load_digits(y, A.mod.r2);
-      mt.mul(y, x, y);                            // Mont(b)
+      mt.load_words(y, A.b + ib * A.wc, A.wc);
     }
-    mt.load_words(x, A.a + ii * A.wc, A.wc, 0);
-    mt.mul(x, x, y);                              // a*b plain
-    mt.canonical(x);
-    mt.store_words(A.out + ii * A.wc, A.wc, x, sm, valid);
+    mt.load_limbs(x, A.mod.r2);
+    mt.mul(y, y, x);                              // Mont(b)
+    mt.load_words(x, A.a + ii * A.wc, A.wc);
+    mt.mul(x, x, y);                              // a*b plain, canonical
+    mt.store_words(A.out + ii * A.wc, A.wc, x, valid);
   }
 }
 
@@ -170,10 +164,8 @@ template <int LPT, int TPI>
 __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_decrypt(DecArgs A) {
   using M = Mont<LPT, TPI>;
   constexpr int IPW = 32 / TPI;
-  extern __shared__ uint32_t smem[];
   M mt;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane / TPI;
-  uint32_t* sm = smem + (warp * IPW + g) * (M::L + 2);
   const long wg = (long)blockIdx.x * (blockDim.x >> 5) + warp, nw = (long)gridDim.x * (blockDim.x >> 5);
   uint32_t* tw = A.tbl + wg * A.tbl_stride;
   const long ntiles = (A.count + IPW - 1) / IPW;
@@ -189,60 +181,45 @@ __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_decrypt(DecArgs A) 
       const HalfDev& H = A.half[h];
       mt.init(H.s2.n, H.s2.np);
       // c mod s^2 in Montgomery form, from the two word halves of c
-      mt.load_words(x, cw, wlo, 0);
-      mt.load_digits(y, H.s2.r2);
+      mt.load_words(x, cw, wlo);
+      mt.load_limbs(y, H.s2.r2);
       mt.mul(x, x, y);
-      mt.load_words(y, cw + wlo, whi, 0);
-      mt.load_digits(z, H.hiR2);
+      mt.load_words(y, cw + wlo, whi);
+      mt.load_limbs(z, H.hiR2);
       mt.mul(y, y, z);
-#pragma unroll
-      for (int k = 0; k < LPT; k++) x[k] += y[k];
-      mt.renorm(x);
+      mt.add_mod(x, x, y);
       run_prog<LPT, TPI>(mt, x, H.prog, H.nprog, tw);   // Mont(c^(s-1) mod s^2)
       mt.set_one(z);
-      mt.mul(x, x, z);
-      mt.canonical(x);                              // u = c^(s-1) mod s^2
+      mt.mul(x, x, z);                              // u = c^(s-1) mod s^2
       // u == 0 happens only when s divides c (never for a real ciphertext); the reference's floor
       // division (0 - 1) // s is then -1, i.e. t = s - 1 (mod s).
       const bool uzero = mt.is_zero(x);
-      mt.decrement(x);                              // u - 1 = s * t
+      mt.sub_mod(x, x, z);                          // u - 1 = s * t
       mt.init(H.s1.n, H.s1.np);
-      mt.mul_quot(x, y, x, z);                      // y <- quotient digits of (u-1)*1 w.r.t. s
-      mt.negate(y);                                 // t = (u - 1) / s
+      mt.mul_quot(x, y, x, z);                      // y <- quotient limbs of (u-1)*1 w.r.t. s
+      mt.neg_R(y);                                  // t = (u - 1) / s
       if (uzero) {
 #pragma unroll
         for (int k = 0; k < LPT; k++) y[k] = mt.n[k];
-        y[0] -= mt.m0 & 1u;
+        if (mt.t == 0) y[0] -= 1u;                  // s is odd: no borrow
       }
-      mt.load_digits(z, H.hsR);
-      mt.mul(x, y, z);
-      mt.canonical(x);                              // ms = t * hs mod s
+      mt.load_limbs(z, H.hsR);
+      mt.mul(x, y, z);                              // ms = t * hs mod s
       if (h == 0) tile_store<LPT>(tw, A.stash_slot, x);
     }
     // x = mq.  CRT recombination: m = mq + q * ((mp - mq) * q_inv mod p)   (operators.py:56)
     mt.init(A.half[0].s1.n, A.half[0].s1.np);       // modulus p
-    mt.load_digits(y, A.half[0].s1.r1);
-    mt.mul(y, x, y);
-    mt.canonical(y);                                // mq mod p
+    mt.load_limbs(y, A.half[0].s1.r1);
+    mt.mul(y, x, y);                                // mq mod p
     tile_load<LPT>(tw, A.stash_slot, z);            // mp
-#pragma unroll
-    for (int k = 0; k < LPT; k++) y[k] = mt.n[k] + (DMASK - y[k]);
-    y[0] += mt.m0 & 1u;
-    mt.normalize(y);                                // p - (mq mod p); the carry out (= R) is dropped
-#pragma unroll
-    for (int k = 0; k < LPT; k++) y[k] += z[k];
-    mt.normalize(y);                                // mp + p - (mq mod p)  in (0, 2p)
-    mt.load_digits(z, A.qinvR);
-    mt.mul(y, y, z);
-    mt.canonical(y);                                // h in [0, p)
+    mt.sub_mod(y, z, y);                            // (mp - mq) mod p
+    mt.load_limbs(z, A.qinvR);
+    mt.mul(y, y, z);                                // h in [0, p)
     mt.init(A.modn.n, A.modn.np);
-    mt.load_digits(z, A.qR);
-    mt.mul(y, y, z);
-    mt.canonical(y);                                // q * h  (< n, exact)
-#pragma unroll
-    for (int k = 0; k < LPT; k++) x[k] += y[k];
-    mt.canonical(x);
-    mt.store_words(A.out + ii * A.wn, A.wn, x, sm, valid);
+    mt.load_limbs(z, A.qR);
+    mt.mul(y, y, z);                                // q * h  (< n, exact)
+    mt.add_mod(x, x, y);                            // mq + q*h  (< n)
+    mt.store_words(A.out + ii * A.wn, A.wn, x, valid);
   }
 }
 

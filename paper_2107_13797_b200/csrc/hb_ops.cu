@@ -26,11 +26,11 @@ inline int Ldig(int cfg) { return kCfgs[cfg].lpt * kCfgs[cfg].tpi; }
 
 #define HB_DISPATCH1(cfg, KERNEL, stream, args)                                      \
   switch (cfg) {                                                                     \
-    case 0: hb::KERNEL<9, 4><<<1, 32, 0, stream>>>(args); break;                     \
-    case 1: hb::KERNEL<18, 4><<<1, 32, 0, stream>>>(args); break;                    \
-    case 2: hb::KERNEL<27, 4><<<1, 32, 0, stream>>>(args); break;                    \
-    case 3: hb::KERNEL<18, 8><<<1, 32, 0, stream>>>(args); break;                    \
-    case 4: hb::KERNEL<27, 8><<<1, 32, 0, stream>>>(args); break;                    \
+    case 0: hb::KERNEL<8, 4><<<1, 32, 0, stream>>>(args); break;                     \
+    case 1: hb::KERNEL<16, 4><<<1, 32, 0, stream>>>(args); break;                    \
+    case 2: hb::KERNEL<24, 4><<<1, 32, 0, stream>>>(args); break;                    \
+    case 3: hb::KERNEL<16, 8><<<1, 32, 0, stream>>>(args); break;                    \
+    case 4: hb::KERNEL<24, 8><<<1, 32, 0, stream>>>(args); break;                    \
     default: return hbi::fail(HB_ERR_UNSUPPORTED, "no limb configuration");          \
   }                                                                                  \
   hbi::g_launches++;
@@ -63,7 +63,7 @@ int invert_batch(hb_ctx* ctx, const uint32_t* val, long count, uint32_t* inv, Sc
     lv_n.push_back(ndst);
   }
   // root
-  const int T = 32 * ((29 * L + 31) / 32 / 32 + 1);
+  const int T = 32 * (L / 32 + 1);
   uint32_t* root = nullptr; uint32_t* words = nullptr; int* status = nullptr;
   CU(sc.get(&root, (size_t)L));
   CU(sc.get(&words, (size_t)T));

@@ -6,7 +6,7 @@
 //   k_product_pass  operators.py:75-83   _k_product
 //   bucket kernels  operators.py:86-94   _k_dot: out_j = prod_t pow_scalar(c_t, k_tj)
 //
-// "Digit form" below means L radix-2^29 digits per number, Montgomery representation (x * R mod N),
+// "Digit form" below means the L 32-bit limbs of a number, Montgomery representation (x * R mod N),
 // stored contiguously: element i lives at base + i * L, lane t of its group owns digits [t*LPT, (t+1)*LPT).
 #pragma once
 #include "hb_ctx.h"
@@ -36,10 +36,10 @@ __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_to_mont(ToMontArgs 
     bool valid = inst < A.count;
     long ii = valid ? inst : A.count - 1;
     uint32_t x[LPT], y[LPT];
-    mt.load_words(x, A.words + ii * A.w, A.w, 0);
-    mt.load_digits(y, A.mod.r2);
+    mt.load_words(x, A.words + ii * A.w, A.w);
+    mt.load_limbs(y, A.mod.r2);
     mt.mul(x, x, y);
-    if (valid) mt.store_digits(A.dig + ii * L, x);
+    if (valid) mt.store_limbs(A.dig + ii * L, x);
   }
 }
 
@@ -59,11 +59,11 @@ __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_pair_up(PairUpArgs 
     bool valid = inst < ndst;
     long j = valid ? inst : ndst - 1;
     uint32_t x[LPT], y[LPT];
-    mt.load_digits(x, A.src + (2 * j) * L);
+    mt.load_limbs(x, A.src + (2 * j) * L);
     bool sib = 2 * j + 1 < A.nsrc;
-    if (sib) mt.load_digits(y, A.src + (2 * j + 1) * L); else mt.load_digits(y, A.mod.r1);
+    if (sib) mt.load_limbs(y, A.src + (2 * j + 1) * L); else mt.load_limbs(y, A.mod.r1);
     mt.mul(x, x, y);
-    if (valid) mt.store_digits(A.dst + j * L, x);
+    if (valid) mt.store_limbs(A.dst + j * L, x);
   }
 }
 
@@ -81,11 +81,11 @@ __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_pair_down(PairDownA
     bool valid = inst < A.nchild;
     long i = valid ? inst : A.nchild - 1;
     uint32_t x[LPT], y[LPT];
-    mt.load_digits(x, A.inv_parent + (i >> 1) * L);
+    mt.load_limbs(x, A.inv_parent + (i >> 1) * L);
     long s = i ^ 1;
-    if (s < A.nchild) mt.load_digits(y, A.val_child + s * L); else mt.load_digits(y, A.mod.r1);
+    if (s < A.nchild) mt.load_limbs(y, A.val_child + s * L); else mt.load_limbs(y, A.mod.r1);
     mt.mul(x, x, y);
-    if (valid) mt.store_digits(A.inv_child + i * L, x);
+    if (valid) mt.store_limbs(A.inv_child + i * L, x);
   }
 }
 
@@ -177,20 +177,19 @@ template <int LPT, int TPI>
 __global__ void __launch_bounds__(32) k_root_inverse(RootInvArgs A) {
   using M = Mont<LPT, TPI>;
   constexpr int L = LPT * TPI;
-  constexpr int K = (29 * L + 31) / 32 / 32 + 1;
+  constexpr int K = L / 32 + 1;
   constexpr int T = 32 * K;
-  __shared__ uint32_t sm[L + 2];
   const int lane = threadIdx.x & 31;
   M mt;
   mt.init(A.mod.n, A.mod.np);
   uint32_t x[LPT], y[LPT];
   // every group works on the same number; group 0's stores are the ones kept
-  mt.load_digits(x, A.root);
+  mt.load_limbs(x, A.root);
   mt.set_one(y);
   mt.mul(x, x, y);
-  mt.canonical(x);                                // plain a
-  // (all groups write identical values to the same shared slots)
-  mt.store_words(A.words, T, x, sm, lane < TPI);
+  // plain a; group 0 writes its limbs, everything above L is zero
+  mt.store_words(A.words, L, x, lane < TPI);
+  for (int k = L + lane; k < T; k += 32) A.words[k] = 0;
   __syncwarp();
   __threadfence_block();
   WarpBig<K> u, v, x1, x2, nn;
@@ -236,10 +235,10 @@ __global__ void __launch_bounds__(32) k_root_inverse(RootInvArgs A) {
   for (int i = 0; i < K; i++) A.words[lane * K + i] = x1.w[i];
   __syncwarp();
   __threadfence_block();
-  mt.load_words(x, A.words, T, 0);
-  mt.load_digits(y, A.mod.r2);
+  mt.load_words(x, A.words, L);
+  mt.load_limbs(y, A.mod.r2);
   mt.mul(x, x, y);                                // Mont(a^-1)
-  if (lane < TPI) mt.store_digits(A.root, x);
+  if (lane < TPI) mt.store_limbs(A.root, x);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -322,8 +321,6 @@ struct PowVarArgs {
 template <int LPT, int TPI>
 __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_powvar(PowVarArgs A) {
   HB_GROUP_PROLOGUE(LPT, TPI)
-  extern __shared__ uint32_t smem[];
-  uint32_t* sm = smem + (warp * IPW + g) * (L + 2);
   M mt;
   mt.init(A.mod.n, A.mod.np);
   uint32_t* tw = A.tbl + wg * A.tbl_stride;
@@ -337,9 +334,9 @@ __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_powvar(PowVarArgs A
     const bool neg = A.neg[ki] != 0;
     uint32_t x[LPT], y[LPT];
     const uint32_t* bp = (neg ? A.base_inv : A.base) + (e / A.c_div) * L;
-    mt.load_digits(y, bp);
+    mt.load_limbs(y, bp);
     // table: slot 0 = Mont(1), slot 1 = b, slot i = b^i
-    mt.load_digits(x, A.mod.r1);
+    mt.load_limbs(x, A.mod.r1);
     tile_store<LPT>(tw, 0, x);
     tile_store<LPT>(tw, 1, y);
 #pragma unroll
@@ -394,8 +391,7 @@ __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_powvar(PowVarArgs A
     }
     mt.set_one(y);
     mt.mul(x, x, y);
-    mt.canonical(x);
-    mt.store_words(A.out + e * A.wc, A.wc, x, sm, valid);
+    mt.store_words(A.out + e * A.wc, A.wc, x, valid);
   }
 }
 
@@ -415,8 +411,6 @@ struct ProductArgs {
 template <int LPT, int TPI>
 __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_product_pass(ProductArgs A) {
   HB_GROUP_PROLOGUE(LPT, TPI)
-  extern __shared__ uint32_t smem[];
-  uint32_t* sm = smem + (warp * IPW + g) * (L + 2);
   M mt;
   mt.init(A.mod.n, A.mod.np);
   const long nitems = A.ngroups * A.parts;
@@ -425,8 +419,8 @@ __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_product_pass(Produc
   uint32_t fix[LPT];
   {
     uint32_t h1[LPT];
-    mt.load_digits(fix, A.mod.r1);     // h_0
-    mt.load_digits(h1, A.mod.r2);      // h_1
+    mt.load_limbs(fix, A.mod.r1);     // h_0
+    mt.load_limbs(h1, A.mod.r2);      // h_1
     long idx = A.clen - 1;
     int top = 63 - __clzll((unsigned long long)(idx | 1));
 #pragma unroll 1
@@ -447,7 +441,7 @@ __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_product_pass(Produc
 #pragma unroll 1
     for (long i = 0; i < A.clen; i++) {
       long t = t0 + i;
-      if (t < A.glen) mt.load_words(y, A.c + (grp * A.gstride + t * A.estride) * A.wc, A.wc, 0);
+      if (t < A.glen) mt.load_words(y, A.c + (grp * A.gstride + t * A.estride) * A.wc, A.wc);
       else mt.set_one(y);
       if (first) {
 #pragma unroll
@@ -458,8 +452,7 @@ __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_product_pass(Produc
       }
     }
     mt.mul(x, x, fix);      // clen - 1 deficits repaired: x * R^clen / R
-    mt.canonical(x);
-    mt.store_words(A.out + it * A.wc, A.wc, x, sm, valid);
+    mt.store_words(A.out + it * A.wc, A.wc, x, valid);
   }
 }
 
@@ -527,7 +520,7 @@ __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_bucket_segments(Seg
   const long nitems = (long)A.d * A.nwin * A.nseg;
   const long ntiles = (nitems + IPW - 1) / IPW;
   uint32_t one[LPT];
-  mt.load_digits(one, A.mod.r1);
+  mt.load_limbs(one, A.mod.r1);
   for (long tile = wg; tile < ntiles; tile += nw) {
     long inst = tile * IPW + g;
     bool valid = inst < nitems;
@@ -549,8 +542,8 @@ __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_bucket_segments(Seg
       uint32_t ent = have ? so[p] : 0u;
       int b = have ? (int)(ent >> 22) : cur;
       bool change = b != cur;
-      if (change && cur >= 0) mt.store_digits(pt + (seg + cur) * L, acc);
-      if (have) mt.load_digits(y, A.cm + (long)(ent & 0x3fffffu) * L);
+      if (change && cur >= 0) mt.store_limbs(pt + (seg + cur) * L, acc);
+      if (have) mt.load_limbs(y, A.cm + (long)(ent & 0x3fffffu) * L);
       else {
 #pragma unroll
         for (int k = 0; k < LPT; k++) y[k] = one[k];
@@ -562,7 +555,7 @@ __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_bucket_segments(Seg
       mt.mul(acc, acc, y);
       cur = b;
     }
-    if (cur >= 0) mt.store_digits(pt + (seg + cur) * L, acc);
+    if (cur >= 0) mt.store_limbs(pt + (seg + cur) * L, acc);
   }
 }
 
@@ -583,7 +576,7 @@ __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_bucket_combine(Comb
   const long nitems = (long)A.d * A.nwin * NB;
   const long ntiles = (nitems + IPW - 1) / IPW;
   uint32_t one[LPT];
-  mt.load_digits(one, A.mod.r1);
+  mt.load_limbs(one, A.mod.r1);
   for (long tile = wg; tile < ntiles; tile += nw) {
     long inst = tile * IPW + g;
     bool valid = inst < nitems;
@@ -610,14 +603,14 @@ __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_bucket_combine(Comb
     for (int k = 0; k < LPT; k++) acc[k] = one[k];
 #pragma unroll 1
     for (long i = 0; i < maxcnt; i++) {
-      if (i < cnt) mt.load_digits(y, pt + (s_lo + i + b) * L);
+      if (i < cnt) mt.load_limbs(y, pt + (s_lo + i + b) * L);
       else {
 #pragma unroll
         for (int k = 0; k < LPT; k++) y[k] = one[k];
       }
       mt.mul(acc, acc, y);
     }
-    if (valid) mt.store_digits(A.bucket + it * L, acc);
+    if (valid) mt.store_limbs(A.bucket + it * L, acc);
   }
 }
 
@@ -644,15 +637,15 @@ __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_bucket_running(Runn
     long j = jw / A.nwin; int w = (int)(jw - j * A.nwin);
     const uint32_t* bk = A.bucket + jw * NB * L;
     uint32_t acc[LPT], tot[LPT], y[LPT];
-    mt.load_digits(acc, A.mod.r1);
-    mt.load_digits(tot, A.mod.r1);
+    mt.load_limbs(acc, A.mod.r1);
+    mt.load_limbs(tot, A.mod.r1);
 #pragma unroll 1
     for (int v = NV - 1; v >= 1; v--) {
-      mt.load_digits(y, bk + (long)(v * 2 + s) * L);
+      mt.load_limbs(y, bk + (long)(v * 2 + s) * L);
       mt.mul(acc, acc, y);
       mt.mul(tot, tot, acc);
     }
-    if (valid) mt.store_digits(A.win + ((j * 2 + s) * A.nwin + w) * L, tot);
+    if (valid) mt.store_limbs(A.win + ((j * 2 + s) * A.nwin + w) * L, tot);
   }
 }
 
@@ -676,15 +669,15 @@ __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_window_horner(Horne
     long it = valid ? inst : nitems - 1;
     const uint32_t* wv = A.win + it * A.nwin * L;
     uint32_t x[LPT], y[LPT];
-    mt.load_digits(x, wv + (long)(A.nwin - 1) * L);
+    mt.load_limbs(x, wv + (long)(A.nwin - 1) * L);
 #pragma unroll 1
     for (int w = A.nwin - 2; w >= 0; w--) {
 #pragma unroll 1
       for (int s = 0; s < A.cbits; s++) mt.mul(x, x, x);
-      mt.load_digits(y, wv + (long)w * L);
+      mt.load_limbs(y, wv + (long)w * L);
       mt.mul(x, x, y);
     }
-    if (valid) mt.store_digits(A.ab + it * L, x);
+    if (valid) mt.store_limbs(A.ab + it * L, x);
   }
 }
 
@@ -702,13 +695,13 @@ __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_fold(FoldArgs A) {
     bool valid = inst < A.count;
     long i = valid ? inst : A.count - 1;
     uint32_t x[LPT], y[LPT];
-    mt.load_digits(x, A.src + i * L);
+    mt.load_limbs(x, A.src + i * L);
 #pragma unroll 1
     for (int r = 1; r < A.nr; r++) {
-      mt.load_digits(y, A.src + r * A.rstride + i * L);
+      mt.load_limbs(y, A.src + r * A.rstride + i * L);
       mt.mul(x, x, y);
     }
-    if (valid) mt.store_digits(A.dst + i * L, x);
+    if (valid) mt.store_limbs(A.dst + i * L, x);
   }
 }
 
@@ -718,8 +711,6 @@ struct FinishArgs { ModDev mod; const uint32_t* ab; const uint32_t* binv; int d;
 template <int LPT, int TPI>
 __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_matvec_finish(FinishArgs A) {
   HB_GROUP_PROLOGUE(LPT, TPI)
-  extern __shared__ uint32_t smem[];
-  uint32_t* sm = smem + (warp * IPW + g) * (L + 2);
   M mt;
   mt.init(A.mod.n, A.mod.np);
   const long ntiles = (A.d + IPW - 1) / IPW;
@@ -728,15 +719,14 @@ __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_matvec_finish(Finis
     bool valid = inst < A.d;
     long j = valid ? inst : A.d - 1;
     uint32_t x[LPT], y[LPT];
-    mt.load_digits(x, A.ab + (j * 2) * L);
+    mt.load_limbs(x, A.ab + (j * 2) * L);
     if (A.binv) {
-      mt.load_digits(y, A.binv + j * L);
+      mt.load_limbs(y, A.binv + j * L);
       mt.mul(x, x, y);
     }
     mt.set_one(y);
     mt.mul(x, x, y);
-    mt.canonical(x);
-    mt.store_words(A.out + j * A.wc, A.wc, x, sm, valid);
+    mt.store_words(A.out + j * A.wc, A.wc, x, valid);
   }
 }
 

@@ -1,0 +1,299 @@
+// Warp-cooperative Montgomery arithmetic in radix 2^32 with hardware carry chains (sm_100a).
+//
+// Arithmetic core of every modular operator on the reference's hot path
+// (/root/reference/pkg/src/hebatch/operators.py:39-94, which delegates to gmpy2.powmod / mpz "*" "%").
+// Nothing here derives from GMP.  The shape follows what the B200 integer pipe measures
+// (profiles/r01_imad_peak2.json, csrc/imad_peak2.cu):
+//
+//   * a 32x32->64 multiply-add (IMAD.WIDE.U32) issues at ~32 lanes/clk/SM whatever its form -- plain,
+//     64-bit accumulating, or with carry-in/carry-out (IMAD.WIDE.U32.X);
+//   * IADD3 / LOP3 / SHF run on another pipe at ~4x that rate.
+//
+// So the multiplier is the only scarce resource and every limb product should be exactly one
+// IMAD.WIDE.U32.X with its addition and carry folded in; full 32-bit limbs minimise the product count
+// (L^2 per operand pass).  A number has L = LPT * TPI limbs, LPT (even) per lane, TPI lanes.  Per lane
+// two arrays of 64-bit accumulators are kept, E[i] on lane columns (2i, 2i+1) and O[i] on (2i+1, 2i+2),
+// so a row a[k] * b_j is one carry chain over E (even k) and one over O (odd k).  After each row the
+// frame moves down one 32-bit column: E and O swap roles, the eliminated low word of each lane goes to
+// the lane below through one shuffle.  Whatever spills past a lane's top column collects in E[H], O[H]
+// and crosses to the lane above once, after the last row.  Validated against Python integers by
+// tools/mont32_model.py.
+//
+// Values are kept canonical: mul() returns a * b / R mod n in [0, n) for a < R, b < n, R = 2^(32 L).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace hb {
+
+constexpr unsigned FULLMASK = 0xffffffffu;
+
+// r = c + a * b, carry out -> CC
+__device__ __forceinline__ uint64_t mac_cc(uint32_t a, uint32_t b, uint64_t c) {
+  uint64_t r;
+  asm volatile("{\n\t.reg .u64 t;\n\tmul.wide.u32 t, %1, %2;\n\tadd.cc.u64 %0, t, %3;\n\t}" : "=l"(r) : "r"(a), "r"(b), "l"(c));
+  return r;
+}
+// r = c + a * b + CC, carry out -> CC
+__device__ __forceinline__ uint64_t macc_cc(uint32_t a, uint32_t b, uint64_t c) {
+  uint64_t r;
+  asm volatile("{\n\t.reg .u64 t;\n\tmul.wide.u32 t, %1, %2;\n\taddc.cc.u64 %0, t, %3;\n\t}" : "=l"(r) : "r"(a), "r"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t add_cc64(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm volatile("add.cc.u64 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t addc_cc64(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm volatile("addc.cc.u64 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t addc64(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm volatile("addc.u64 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint32_t add_cc32(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm volatile("add.cc.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+__device__ __forceinline__ uint32_t addc_cc32(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm volatile("addc.cc.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+__device__ __forceinline__ uint32_t addc32(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm volatile("addc.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+__device__ __forceinline__ uint32_t lo32(uint64_t v) { return (uint32_t)v; }
+__device__ __forceinline__ uint32_t hi32(uint64_t v) { return (uint32_t)(v >> 32); }
+
+template <int LPT, int TPI>
+struct Mont {
+  static_assert(LPT >= 4 && LPT % 2 == 0, "LPT must be even and at least 4");
+  static_assert(TPI >= 1 && TPI <= 32 && (TPI & (TPI - 1)) == 0, "TPI must be a power of two");
+  static constexpr int H = LPT / 2;
+  static constexpr int L = LPT * TPI;
+  static constexpr uint32_t GM = TPI == 32 ? 0xffffffffu : ((1u << TPI) - 1u);
+
+  uint32_t n[LPT];     // modulus limbs owned by this lane
+  uint32_t np;         // -n^-1 mod 2^32
+  int t;               // lane index inside the group
+  int gshift;          // position of the group's lane 0 in the warp
+  bool top;            // this lane holds the most significant limbs
+
+  __device__ __forceinline__ void init(const uint32_t* __restrict__ n_limbs, uint32_t np_) {
+    const int lane = threadIdx.x & 31;
+    t = lane & (TPI - 1);
+    gshift = lane & ~(TPI - 1);
+    top = t == TPI - 1;
+    np = np_;
+#pragma unroll
+    for (int i = 0; i < LPT; i++) n[i] = n_limbs[t * LPT + i];
+  }
+
+  // E, O += v * x : one carry chain per accumulator array (H multiply-adds each)
+  __device__ __forceinline__ void mac_row(uint64_t (&E)[H + 1], uint64_t (&O)[H + 1], const uint32_t (&v)[LPT],
+                                          uint32_t x) const {
+    E[0] = mac_cc(v[0], x, E[0]);
+#pragma unroll
+    for (int i = 1; i < H; i++) E[i] = macc_cc(v[2 * i], x, E[i]);
+    E[H] = addc64(E[H], 0);
+    O[0] = mac_cc(v[1], x, O[0]);
+#pragma unroll
+    for (int i = 1; i < H; i++) O[i] = macc_cc(v[2 * i + 1], x, O[i]);
+    O[H] = addc64(O[H], 0);
+  }
+
+  // Resolves pending single-bit carries between lanes: g (0/1) leaves this lane; returns the carry that
+  // leaves the top lane (same value on every lane of the group).
+  __device__ __forceinline__ uint32_t lane_carries(uint32_t (&r)[LPT], uint32_t g, uint32_t cin0 = 0u) const {
+    uint32_t all = r[0];
+#pragma unroll
+    for (int i = 1; i < LPT; i++) all &= r[i];
+    const uint32_t G = (__ballot_sync(FULLMASK, g != 0) >> gshift) & GM;
+    const uint32_t P = (__ballot_sync(FULLMASK, all == 0xffffffffu) >> gshift) & GM;
+    const uint64_t S = (uint64_t)P + ((uint64_t)G << 1) + cin0;   // cin0: carry into the lowest lane
+    const uint32_t C = (uint32_t)S ^ P;              // bit t: carry entering lane t
+    const uint32_t c = (C >> t) & 1u;
+    r[0] = add_cc32(r[0], c);
+#pragma unroll
+    for (int i = 1; i < LPT; i++) r[i] = addc_cc32(r[i], 0);
+    return (uint32_t)(S >> TPI) & 1u;
+  }
+
+  // r = a + b + cin0 as L-limb integers (cin0 enters at the lowest limb); returns the carry out of the number
+  __device__ __forceinline__ uint32_t add_raw(uint32_t (&r)[LPT], const uint32_t (&a)[LPT],
+                                              const uint32_t (&b)[LPT], uint32_t cin0) const {
+    r[0] = add_cc32(a[0], b[0]);
+#pragma unroll
+    for (int i = 1; i < LPT; i++) r[i] = addc_cc32(a[i], b[i]);
+    const uint32_t g = addc32(0, 0);
+    return lane_carries(r, g, cin0);
+  }
+
+  // r = a - b as L-limb integers (mod R); returns 1 when a >= b (no borrow)
+  __device__ __forceinline__ uint32_t sub_raw(uint32_t (&r)[LPT], const uint32_t (&a)[LPT],
+                                              const uint32_t (&b)[LPT]) const {
+    uint32_t nb[LPT];
+#pragma unroll
+    for (int i = 0; i < LPT; i++) nb[i] = ~b[i];
+    return add_raw(r, a, nb, 1u);
+  }
+
+  // r in [0, 2n) given as limbs plus an overflow bit  ->  [0, n)
+  __device__ __forceinline__ void cond_sub(uint32_t (&r)[LPT], uint32_t hi) const {
+    uint32_t d[LPT];
+    const uint32_t ge = sub_raw(d, r, n);
+    if (hi | ge) {
+#pragma unroll
+      for (int i = 0; i < LPT; i++) r[i] = d[i];
+    }
+  }
+
+  __device__ __forceinline__ void add_mod(uint32_t (&r)[LPT], const uint32_t (&a)[LPT], const uint32_t (&b)[LPT]) const {
+    const uint32_t hi = add_raw(r, a, b, 0u);
+    cond_sub(r, hi);
+  }
+  __device__ __forceinline__ void sub_mod(uint32_t (&r)[LPT], const uint32_t (&a)[LPT], const uint32_t (&b)[LPT]) const {
+    uint32_t d[LPT], s[LPT];
+    const uint32_t ge = sub_raw(d, a, b);
+    add_raw(s, d, n, 0u);               // unconditional: no warp collective inside a group-divergent branch
+#pragma unroll
+    for (int i = 0; i < LPT; i++) r[i] = ge ? d[i] : s[i];
+  }
+  // r = (R - r) mod R
+  __device__ __forceinline__ void neg_R(uint32_t (&r)[LPT]) const {
+    uint32_t z[LPT], s[LPT];
+#pragma unroll
+    for (int i = 0; i < LPT; i++) { z[i] = 0; s[i] = r[i]; }
+    sub_raw(r, z, s);
+  }
+  __device__ __forceinline__ void set_one(uint32_t (&r)[LPT]) const {
+#pragma unroll
+    for (int i = 0; i < LPT; i++) r[i] = 0;
+    r[0] = (t == 0) ? 1u : 0u;
+  }
+  __device__ __forceinline__ bool is_zero(const uint32_t (&r)[LPT]) const {
+    uint32_t any = r[0];
+#pragma unroll
+    for (int i = 1; i < LPT; i++) any |= r[i];
+    return ((__ballot_sync(FULLMASK, any != 0) >> gshift) & GM) == 0;
+  }
+
+  __device__ __forceinline__ void mul(uint32_t (&r)[LPT], const uint32_t (&a)[LPT], const uint32_t (&b)[LPT]) const {
+    uint32_t unused[LPT];
+    mul_impl<false>(r, a, b, unused);
+  }
+  // mul() that also returns the Montgomery quotient Q = -(a*b) * n^-1 mod R (lane t gets its LPT limbs).
+  // When a*b is a multiple of n:  a*b / n = (R - Q) mod R.
+  __device__ __forceinline__ void mul_quot(uint32_t (&r)[LPT], uint32_t (&qd)[LPT], const uint32_t (&a)[LPT],
+                                           const uint32_t (&b)[LPT]) const {
+    mul_impl<true>(r, a, b, qd);
+  }
+
+  template <bool COLLECT>
+  __device__ __forceinline__ void mul_impl(uint32_t (&r)[LPT], const uint32_t (&a)[LPT], const uint32_t (&b)[LPT],
+                                           uint32_t (&qd)[LPT]) const {
+    uint64_t E[H + 1], O[H + 1];
+#pragma unroll
+    for (int i = 0; i <= H; i++) { E[i] = 0; O[i] = 0; }
+    // what is left of an eliminated column (up to 33 bits) waits here for the next row instead of being
+    // rippled through the accumulators
+    uint32_t pend_lo = 0, pend_hi = 0;
+#pragma unroll 1
+    for (int s = 0; s < TPI; s++) {
+#pragma unroll
+      for (int i = 0; i < LPT; i++) {
+        const uint32_t bj = __shfl_sync(FULLMASK, b[i], s, TPI);
+        mac_row(E, O, a, bj);
+        uint32_t q = (lo32(E[0]) + pend_lo) * np;
+        q = __shfl_sync(FULLMASK, q, 0, TPI);
+        if (COLLECT) { if (s == t) qd[i] = q; }
+        mac_row(E, O, n, q);
+        // column 0 = E[0] + pend: its low word is zero on lane 0 and goes to the lane below elsewhere
+        const uint32_t vlo = add_cc32(lo32(E[0]), pend_lo);
+        const uint32_t vhi = addc_cc32(hi32(E[0]), pend_hi);
+        const uint32_t vtop = addc32(0, 0);
+        uint32_t recv = __shfl_down_sync(FULLMASK, vlo, 1, TPI);
+        recv = top ? 0u : recv;
+        pend_lo = vhi;
+        pend_hi = vtop;
+        // frame moves down one column: E <- O, O[k] <- E[k + 1], the received word lands on the top column
+        uint64_t F[H + 1];
+#pragma unroll
+        for (int k = 0; k <= H; k++) F[k] = O[k];
+#pragma unroll
+        for (int k = 0; k < H - 1; k++) O[k] = E[k + 1];
+        O[H - 1] = add_cc64(E[H], (uint64_t)recv);
+        O[H] = addc64(0, 0);
+#pragma unroll
+        for (int k = 0; k <= H; k++) E[k] = F[k];
+      }
+    }
+    // fold the pending column back in (once per multiplication)
+    E[0] = add_cc64(E[0], ((uint64_t)pend_hi << 32) | pend_lo);
+#pragma unroll
+    for (int k = 1; k < H; k++) E[k] = addc_cc64(E[k], 0);
+    E[H] = addc64(E[H], 0);
+    // lane value = sum E[i] 2^(64 i) + sum O[i] 2^(64 i + 32): LPT + 3 words w[]
+    uint32_t w[LPT + 3];
+    w[0] = lo32(E[0]);
+    w[1] = add_cc32(hi32(E[0]), lo32(O[0]));
+#pragma unroll
+    for (int i = 1; i <= H; i++) {
+      w[2 * i] = addc_cc32(lo32(E[i]), hi32(O[i - 1]));
+      w[2 * i + 1] = addc_cc32(hi32(E[i]), lo32(O[i]));
+    }
+    w[LPT + 2] = addc32(hi32(O[H]), 0);
+    // the three words above the lane's top column belong to the lane above
+    uint32_t u0 = __shfl_up_sync(FULLMASK, w[LPT], 1, TPI);
+    uint32_t u1 = __shfl_up_sync(FULLMASK, w[LPT + 1], 1, TPI);
+    uint32_t u2 = __shfl_up_sync(FULLMASK, w[LPT + 2], 1, TPI);
+    if (t == 0) { u0 = 0; u1 = 0; u2 = 0; }
+    r[0] = add_cc32(w[0], u0);
+    r[1] = addc_cc32(w[1], u1);
+    r[2] = addc_cc32(w[2], u2);
+#pragma unroll
+    for (int i = 3; i < LPT; i++) r[i] = addc_cc32(w[i], 0);
+    const uint32_t g = addc32(0, 0);
+    uint32_t hi = lane_carries(r, g);
+    // top lane: its own overflow word (value < 2n < 2R, so at most one bit)
+    const uint32_t topw = __shfl_sync(FULLMASK, w[LPT], TPI - 1, TPI);
+    hi |= topw;
+    cond_sub(r, hi);
+  }
+
+  // limbs [t*LPT, (t+1)*LPT) of the little-endian word array w[0..nwords) (zero beyond it)
+  __device__ __forceinline__ void load_words(uint32_t (&r)[LPT], const uint32_t* __restrict__ w, int nwords) const {
+#pragma unroll
+    for (int i = 0; i < LPT; i++) {
+      const int k = t * LPT + i;
+      r[i] = k < nwords ? w[k] : 0u;
+    }
+  }
+  __device__ __forceinline__ void store_words(uint32_t* __restrict__ w, int nwords, const uint32_t (&r)[LPT],
+                                              bool valid = true) const {
+#pragma unroll
+    for (int i = 0; i < LPT; i++) {
+      const int k = t * LPT + i;
+      if (valid && k < nwords) w[k] = r[i];
+    }
+  }
+  // full L-limb arrays (constants, scratch)
+  __device__ __forceinline__ void load_limbs(uint32_t (&r)[LPT], const uint32_t* __restrict__ d) const {
+#pragma unroll
+    for (int i = 0; i < LPT; i++) r[i] = d[t * LPT + i];
+  }
+  __device__ __forceinline__ void store_limbs(uint32_t* __restrict__ d, const uint32_t (&r)[LPT]) const {
+#pragma unroll
+    for (int i = 0; i < LPT; i++) d[t * LPT + i] = r[i];
+  }
+};
+
+}  // namespace hb

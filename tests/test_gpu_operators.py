@@ -357,7 +357,7 @@ def test_backend_run_contract(okeys):
     items = [(0, 0), (1, 1), (0, 1)]
     assert be.run(ops._k_dot, (ok.n, ok.n2, ok.neg_band, rows, cols), items) == ho.k_dot(ok, rows, cols, items)
     assert be.run(ops._k_encode, (pk, -8), [1.5, -2.25]) == [ho.encode(ok, v, -8)[0] for v in (1.5, -2.25)]
-    assert be.run(ops._k_decode, (pk, -8), [384, ok.n - 576]) == [1.5, -2.25]
+    assert be.run(ops._k_decode, (pk, -8), [ho.encode(ok, v, -8)[0] for v in (1.5, -2.25)]) == [1.5, -2.25]
     assert be.run(ops._k_add, ok.n2, []) == []
 
 
