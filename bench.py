@@ -326,8 +326,9 @@ def run_b200(args):
     enc_s = enc_ms * 1e-3 / args.steps            # average k_encrypt launch duration (one launch per step)
     achieved = LP_ENCRYPT * count / enc_s
     roofline = {
-        "bound": "imad", "kernel": "k_encrypt<18,8>", "achieved": achieved / 1e12, "peak": peak / 1e12,
-        "unit": "TLP/s (1e12 32x32->64 limb products per second)", "frac": achieved / peak, "traffic": None,
+        "bound": "imad", "kernel": "k_encrypt<16,8>", "achieved": achieved / 1e12, "peak": peak / 1e12,
+        "unit": "TLP/s (1e12 32x32->64 limb products per second)", "frac": achieved / peak,
+        "traffic": _ncu_traffic_per_element() * count if _ncu_traffic_per_element() else None,
         "peak_source": peak_src,
         "note": "integer-multiply bound, not HBM: algorithmic bytes per encrypt are 1 KiB against 8.4e7 limb products",
         "hbm": {"achieved_gbs": count * (2 * wn + wc) * 4 / enc_s / 1e9, "peak_gbs": _hbm_peak()},
@@ -354,6 +355,18 @@ def run_b200(args):
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+def _ncu_traffic_per_element():
+    """dram bytes read + written per encrypted element, from the committed ncu --set full capture of k_encrypt
+    (profiles/r01_ncu_summary.json; the capture ran 37888 elements)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_summary.json")) as fh:
+            enc = json.load(fh)["encrypt"]
+        mb = float(enc["dram__bytes_read.sum"]["value"]) + float(enc["dram__bytes_write.sum"]["value"])
+        return mb * 1e6 / 37888
+    except Exception:
+        return None
 
 
 def _hbm_peak():

@@ -83,11 +83,23 @@ int hb_powscalar(hb_ctx* ctx, const uint32_t* c, const uint32_t* k, uint32_t* ou
  * axis=None: (1, count, 0, 1); axis=0 of rows x cols: (cols, rows, 1, cols); axis=1: (rows, cols, cols, 1). */
 int hb_product(hb_ctx* ctx, const uint32_t* c, uint32_t* out, int64_t ngroups, int64_t glen,
                int64_t gstride, int64_t estride, void* stream);
+/* out[0] = prod_i r[i] mod n^2 for plaintext-width values r (count x pt words).  gcd(out, n) = 1 iff every
+ * r[i] is a unit mod n: the batched form of draw_unit's gcd test (paillier.py:176-177). */
+int hb_unit_product(hb_ctx* ctx, const uint32_t* r, uint32_t* out, int64_t count, void* stream);
 /* _k_dot / batch_matmul, operators.py:86-94,294-317: c is rows x inner ciphertexts, k is inner x d
  * plaintext residues (row-major), out is rows x d:  out[i][j] = prod_t pow_scalar(c[i][t], k[t][j]).
  * Scalars whose magnitude fits 64 bits take the bucket (Pippenger) path; wider ones a generic path. */
 int hb_matvec(hb_ctx* ctx, const uint32_t* c, const uint32_t* k, uint32_t* out, int64_t rows,
               int64_t inner, int64_t d, void* stream);
+
+/* Row-sharded form of hb_matvec for several GPUs: each rank reduces its own rows to d
+ * pairs (A_j, B_j) -- products over the non-negative and the negative scalars -- written as 2*d plain
+ * ciphertext words [d][2][ct words]; the ranks all-gather those (d KiB-sized messages) and every rank (or the
+ * root) combines nranks such blocks: out[j] = (prod_r A_rj) * (prod_r B_rj)^-1.  Exact and commutative, so
+ * the bits equal the single-GPU hb_matvec. */
+int hb_matvec_partial(hb_ctx* ctx, const uint32_t* c, const uint32_t* k, uint32_t* ab_out, int64_t inner,
+                      int64_t d, void* stream);
+int hb_matvec_combine(hb_ctx* ctx, const uint32_t* ab_all, int nranks, uint32_t* out, int64_t d, void* stream);
 
 /* ---- fixed-point codec (encoding.py:54-101), shared exponent per call ------------------------------
  * *first_bad is a DEVICE int64 the caller initialises to -1; it receives the smallest element index that
@@ -100,6 +112,14 @@ int hb_decode_f64(hb_ctx* ctx, const uint32_t* m, int exponent, double* values_o
 /* ---- host-buffer convenience path (pinned staging, side streams) --------------------------------*/
 int hb_encrypt_host(hb_ctx* ctx, const uint32_t* m, const uint32_t* r, uint32_t* out, int64_t count);
 int hb_decrypt_host(hb_ctx* ctx, const uint32_t* c, uint32_t* m_out, int64_t count);
+
+/* ---- obfuscation-factor stream (host code) -----------------------------------------------------
+ * `count` values of random.Random.randrange(1, n), bit-identical to CPython: `state` are the 624 words and
+ * `*index` the position of rng.getstate()[1]; both are advanced so the caller can setstate() afterwards.
+ * Replaces the randrange half of paillier.draw_unit (paillier.py:173-178); the gcd(r, n) = 1 half is checked
+ * by the caller on the whole batch.  out: count x wn words. */
+int hb_mt19937_randrange1(uint32_t* state, int* index, const uint32_t* n_words, int wn, int64_t count,
+                          uint32_t* out);
 
 /* ---- instrumentation ----------------------------------------------------------------------------*/
 /* Number of kernels this library has launched since load (all contexts). */

@@ -49,9 +49,13 @@ SIGNATURES = {
     "hb_lift_mulmod": (_int, [_vp, _vp, _vp, _vp, _i64, _int, _vp]),
     "hb_powscalar": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _int, _vp]),
     "hb_product": (_int, [_vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp]),
+    "hb_unit_product": (_int, [_vp, _vp, _vp, _i64, _vp]),
     "hb_matvec": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _vp]),
+    "hb_matvec_partial": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _vp]),
+    "hb_matvec_combine": (_int, [_vp, _vp, _int, _vp, _i64, _vp]),
     "hb_encode_f64": (_int, [_vp, _vp, _int, _vp, _i64, _vp, _vp]),
     "hb_decode_f64": (_int, [_vp, _vp, _int, _vp, _i64, _vp, _vp]),
+    "hb_mt19937_randrange1": (_int, [_vp, _vp, _vp, _int, _i64, _vp]),
     "hb_encrypt_host": (_int, [_vp, _vp, _vp, _vp, _i64]),
     "hb_decrypt_host": (_int, [_vp, _vp, _vp, _i64]),
 }

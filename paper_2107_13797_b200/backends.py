@@ -110,10 +110,63 @@ class CudaBackend(ExecutionBackend):
                                             self._stream()))
         return out
 
+    def unit_product(self, n: int, r: device.WordArray) -> int:
+        """prod r[i] mod n^2 as a Python int (one value crosses back)."""
+        ctx = device.context_for(n)
+        out = device.WordArray.empty_device(1, ctx.wc)
+        _native.check(self.lib().hb_unit_product(ctx.handle, r.ptr(), out.ptr(), r.count, self._stream()))
+        return out.ints()[0]
+
+    def draw_units(self, n: int, count: int, rng) -> device.WordArray:
+        """`count` obfuscation factors, bit-identical to [draw_unit(n, rng) for _ in range(count)]
+        (paillier.py:173-178): the randrange stream comes from the native MT19937 replay of the generator's
+        state, the gcd test is one product on the GPU and one gcd.  Falls back to the per-element loop for
+        generators that are not exactly random.Random, for small moduli, and if the batch gcd fails."""
+        import ctypes
+        import math
+        import random as _random
+        import numpy as np
+        from .paillier import draw_unit
+        wn = (n.bit_length() + 31) // 32
+        if count == 0:
+            return device.WordArray.from_ints((), wn)
+        if type(rng) is not _random.Random or n.bit_length() < 256 or count < 4:
+            return device.WordArray.from_ints([draw_unit(n, rng) for _ in range(count)], wn)
+        saved = rng.getstate()
+        version, internal, gauss = saved
+        state = np.array(internal[:624], dtype=np.uint32)
+        index = ctypes.c_int(internal[624])
+        n_words = device.ints_to_words([n], wn)
+        out = np.empty((count, wn), dtype=np.uint32)
+        _native.check(self.lib().hb_mt19937_randrange1(state.ctypes.data, ctypes.byref(index), n_words.ctypes.data,
+                                                       wn, count, out.ctypes.data))
+        words = device.WordArray.from_numpy(out)
+        if math.gcd(self.unit_product(n, words), n) != 1:
+            rng.setstate(saved)                       # a non-unit was drawn: redo it the slow, exact way
+            return device.WordArray.from_ints([draw_unit(n, rng) for _ in range(count)], wn)
+        rng.setstate((version, tuple(int(v) for v in state) + (index.value,), gauss))
+        return words
+
     def matvec(self, n: int, c: device.WordArray, k: device.WordArray, rows: int, inner: int, d: int) -> device.WordArray:
         ctx = device.context_for(n)
         out = device.WordArray.empty_device(rows * d, ctx.wc)
         _native.check(self.lib().hb_matvec(ctx.handle, c.ptr(), k.ptr(), out.ptr(), rows, inner, d, self._stream()))
+        return out
+
+    def matvec_partial(self, n: int, c: device.WordArray, k: device.WordArray, inner: int, d: int) -> device.WordArray:
+        """This rank's rows reduced to d pairs (A_j, B_j): [2 d, wc] plain words (sharding.sharded_matmul)."""
+        ctx = device.context_for(n)
+        out = device.WordArray.empty_device(2 * d, ctx.wc)
+        if inner == 0:
+            one = [1] * (2 * d)
+            return device.WordArray.from_ints(one, ctx.wc)
+        _native.check(self.lib().hb_matvec_partial(ctx.handle, c.ptr(), k.ptr(), out.ptr(), inner, d, self._stream()))
+        return out
+
+    def matvec_combine(self, n: int, ab_all: device.WordArray, nranks: int, d: int) -> device.WordArray:
+        ctx = device.context_for(n)
+        out = device.WordArray.empty_device(d, ctx.wc)
+        _native.check(self.lib().hb_matvec_combine(ctx.handle, ab_all.ptr(), nranks, out.ptr(), d, self._stream()))
         return out
 
     def encode_f64(self, n: int, values, exponent: int) -> device.WordArray:

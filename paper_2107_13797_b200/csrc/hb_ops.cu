@@ -158,7 +158,7 @@ int powscalar_impl(hb_ctx* ctx, const uint32_t* c, long ncipher, long c_div, con
   return HB_OK;
 }
 
-int product_impl(hb_ctx* ctx, const uint32_t* c, uint32_t* out, long ngroups, long glen, long gstride,
+int product_impl(hb_ctx* ctx, const uint32_t* c, int win, uint32_t* out, long ngroups, long glen, long gstride,
                  long estride, cudaStream_t stream) {
   const int cfg = ctx->cfg_pub;
   Scratch sc(stream);
@@ -178,22 +178,22 @@ int product_impl(hb_ctx* ctx, const uint32_t* c, uint32_t* out, long ngroups, lo
     Launch l = plan(ctx, cfg, ngroups * parts);
     hb::ProductArgs A;
     A.mod = dev_mod(ctx->d_pub, ctx->mod_n2);
-    A.c = src; A.wc = ctx->wc; A.ngroups = ngroups; A.glen = glen; A.gstride = gstride; A.estride = estride;
+    A.c = src; A.wc = ctx->wc; A.win = win; A.ngroups = ngroups; A.glen = glen; A.gstride = gstride; A.estride = estride;
     A.parts = parts; A.clen = clen; A.out = dst;
     HB_DISPATCH(cfg, k_product_pass, l, stream, A)
     CU(cudaGetLastError());
     if (parts == 1) break;
-    src = dst; glen = parts; gstride = parts; estride = 1;
+    src = dst; glen = parts; gstride = parts; estride = 1; win = ctx->wc;
   }
   return HB_OK;
 }
 
-int matvec_row(hb_ctx* ctx, const uint32_t* c, const PrepOut& pr, uint32_t* out, long inner, int d,
-               cudaStream_t stream) {
+// Bucket-method core for one encrypted row: ab[j] = (A_j, B_j) in digit form, [d][2][L], allocated from sc.
+int matvec_ab(hb_ctx* ctx, const uint32_t* c, const PrepOut& pr, long inner, int d, Scratch& sc,
+              cudaStream_t stream, uint32_t** ab_out) {
   const int cfg = ctx->cfg_pub;
   const int L = Ldig(cfg);
   hb::ModDev mod = dev_mod(ctx->d_pub, ctx->mod_n2);
-  Scratch sc(stream);
   int cbits = inner >= 4096 ? 8 : inner >= 1024 ? 7 : inner >= 256 ? 6 : inner >= 64 ? 5 : inner >= 16 ? 3 : 2;
   const int maxbits = std::max(pr.maxbits, 1);
   const int nwin = (maxbits + cbits - 1) / cbits;
@@ -236,23 +236,41 @@ int matvec_row(hb_ctx* ctx, const uint32_t* c, const PrepOut& pr, uint32_t* out,
     hb::HornerArgs A{mod, win, d, nwin, cbits, ab};
     HB_DISPATCH(cfg, k_window_horner, l, stream, A)
   }
+  CU(cudaGetLastError());
+  *ab_out = ab;
+  return HB_OK;
+}
+
+// out[j] = A_j * B_j^-1 as plain words (invert = false: B_j is known to be 1)
+int matvec_finish(hb_ctx* ctx, const uint32_t* ab, bool invert, int d, uint32_t* out, Scratch& sc,
+                  cudaStream_t stream) {
+  const int cfg = ctx->cfg_pub;
+  const int L = Ldig(cfg);
+  hb::ModDev mod = dev_mod(ctx->d_pub, ctx->mod_n2);
   uint32_t* binv = nullptr;
-  if (pr.nneg > 0) {
+  if (invert) {
     uint32_t* bden = nullptr;
     CU(sc.get(&bden, (size_t)d * L));
     CU(sc.get(&binv, (size_t)d * L));
     hb::k_gather_b<<<(unsigned)(((long)d * L + 255) / 256), 256, 0, stream>>>(ab, bden, d, L);
     g_launches++;
-    rc = invert_batch(ctx, bden, d, binv, sc, stream);
+    int rc = invert_batch(ctx, bden, d, binv, sc, stream);
     if (rc) return rc;
   }
-  {
-    Launch l = plan(ctx, cfg, d);
-    hb::FinishArgs A{mod, ab, binv, d, out, ctx->wc};
-    HB_DISPATCH(cfg, k_matvec_finish, l, stream, A)
-  }
+  Launch l = plan(ctx, cfg, d);
+  hb::FinishArgs A{mod, ab, binv, d, out, ctx->wc};
+  HB_DISPATCH(cfg, k_matvec_finish, l, stream, A)
   CU(cudaGetLastError());
   return HB_OK;
+}
+
+int matvec_row(hb_ctx* ctx, const uint32_t* c, const PrepOut& pr, uint32_t* out, long inner, int d,
+               cudaStream_t stream) {
+  Scratch sc(stream);
+  uint32_t* ab = nullptr;
+  int rc = matvec_ab(ctx, c, pr, inner, d, sc, stream, &ab);
+  if (rc) return rc;
+  return matvec_finish(ctx, ab, pr.nneg > 0, d, out, sc, stream);
 }
 
 }  // namespace
@@ -274,7 +292,14 @@ int hb_product(hb_ctx* ctx, const uint32_t* c, uint32_t* out, int64_t ngroups, i
   if (ngroups < 0 || glen < 1) return fail(HB_ERR_ARG, "bad group shape");
   if (ngroups == 0) return HB_OK;
   CU(cudaSetDevice(ctx->device));
-  return product_impl(ctx, c, out, ngroups, glen, gstride, estride, (cudaStream_t)stream_);
+  return product_impl(ctx, c, ctx->wc, out, ngroups, glen, gstride, estride, (cudaStream_t)stream_);
+}
+
+int hb_unit_product(hb_ctx* ctx, const uint32_t* r, uint32_t* out, int64_t count, void* stream_) {
+  if (!ctx || !r || !out) return fail(HB_ERR_ARG, "null pointer");
+  if (count < 1) return fail(HB_ERR_ARG, "bad count");
+  CU(cudaSetDevice(ctx->device));
+  return product_impl(ctx, r, ctx->wn, out, 1, count, 0, 1, (cudaStream_t)stream_);
 }
 
 int hb_matvec(hb_ctx* ctx, const uint32_t* c, const uint32_t* k, uint32_t* out, int64_t rows,
@@ -303,10 +328,73 @@ int hb_matvec(hb_ctx* ctx, const uint32_t* c, const uint32_t* k, uint32_t* out, 
     CU(sc.get(&terms, (size_t)inner * d * ctx->wc));
     rc = powscalar_impl(ctx, c + i * inner * ctx->wc, inner, d, k, inner * d, 0, terms, inner * d, stream);
     if (rc) return rc;
-    rc = product_impl(ctx, terms, out + i * d * ctx->wc, d, inner, 1, d, stream);
+    rc = product_impl(ctx, terms, ctx->wc, out + i * d * ctx->wc, d, inner, 1, d, stream);
     if (rc) return rc;
   }
   return HB_OK;
+}
+
+// ---- row-sharded matvec: per-rank partials, exchanged as plain words, combined after the gather --------
+int hb_matvec_partial(hb_ctx* ctx, const uint32_t* c, const uint32_t* k, uint32_t* ab_out, int64_t inner,
+                      int64_t d, void* stream_) {
+  if (!ctx || !c || !k || !ab_out) return fail(HB_ERR_ARG, "null pointer");
+  if (inner < 1 || d < 1) return fail(HB_ERR_ARG, "bad matrix shape");
+  if (inner >= (1 << 22)) return fail(HB_ERR_ARG, "inner dimension must be below 2^22 per call");
+  cudaStream_t stream = (cudaStream_t)stream_;
+  CU(cudaSetDevice(ctx->device));
+  const int cfg = ctx->cfg_pub;
+  Scratch sc(stream);
+  PrepOut pr;
+  int rc = scalar_prep(ctx, k, inner * d, inner, d, 1, 0, sc, stream, &pr);
+  if (rc) return rc;
+  if (pr.maxbits <= 64) {
+    uint32_t* ab = nullptr;
+    rc = matvec_ab(ctx, c, pr, inner, (int)d, sc, stream, &ab);
+    if (rc) return rc;
+    Launch l = plan(ctx, cfg, 2 * d);
+    hb::FromMontArgs A{dev_mod(ctx->d_pub, ctx->mod_n2), ab, 2 * d, ab_out, ctx->wc};
+    HB_DISPATCH(cfg, k_from_mont, l, stream, A)
+    CU(cudaGetLastError());
+    return HB_OK;
+  }
+  // wide scalars: the generic path already folds the inverses in; A_j = result, B_j = 1
+  uint32_t *terms = nullptr, *col = nullptr;
+  CU(sc.get(&terms, (size_t)inner * d * ctx->wc));
+  CU(sc.get(&col, (size_t)d * ctx->wc));
+  rc = powscalar_impl(ctx, c, inner, d, k, inner * d, 0, terms, inner * d, stream);
+  if (rc) return rc;
+  rc = product_impl(ctx, terms, ctx->wc, col, d, inner, 1, d, stream);
+  if (rc) return rc;
+  CU(cudaMemsetAsync(ab_out, 0, (size_t)2 * d * ctx->wc * 4, stream));
+  CU(cudaMemcpy2DAsync(ab_out, (size_t)2 * ctx->wc * 4, col, (size_t)ctx->wc * 4, (size_t)ctx->wc * 4, d,
+                       cudaMemcpyDeviceToDevice, stream));
+  std::vector<uint32_t> ones((size_t)d * ctx->wc, 0);
+  for (int64_t j = 0; j < d; j++) ones[(size_t)j * ctx->wc] = 1;
+  CU(cudaMemcpy2DAsync(ab_out + ctx->wc, (size_t)2 * ctx->wc * 4, ones.data(), (size_t)ctx->wc * 4,
+                       (size_t)ctx->wc * 4, d, cudaMemcpyHostToDevice, stream));
+  CU(cudaStreamSynchronize(stream));     // `ones` lives on this stack frame
+  return HB_OK;
+}
+
+int hb_matvec_combine(hb_ctx* ctx, const uint32_t* ab_all, int nranks, uint32_t* out, int64_t d, void* stream_) {
+  if (!ctx || !ab_all || !out) return fail(HB_ERR_ARG, "null pointer");
+  if (nranks < 1 || d < 1) return fail(HB_ERR_ARG, "bad shape");
+  cudaStream_t stream = (cudaStream_t)stream_;
+  CU(cudaSetDevice(ctx->device));
+  const int cfg = ctx->cfg_pub;
+  const int L = Ldig(cfg);
+  Scratch sc(stream);
+  uint32_t *dig = nullptr, *ab = nullptr;
+  const long per = 2 * d;
+  CU(sc.get(&dig, (size_t)nranks * per * L));
+  CU(sc.get(&ab, (size_t)per * L));
+  int rc = to_mont(ctx, ab_all, ctx->wc, dig, (long)nranks * per, stream);
+  if (rc) return rc;
+  Launch l = plan(ctx, cfg, per);
+  hb::FoldArgs A{dev_mod(ctx->d_pub, ctx->mod_n2), dig, per * L, nranks, per, ab};
+  HB_DISPATCH(cfg, k_fold, l, stream, A)
+  CU(cudaGetLastError());
+  return matvec_finish(ctx, ab, true, (int)d, out, sc, stream);
 }
 
 }  // extern "C"

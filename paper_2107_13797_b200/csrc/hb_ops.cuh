@@ -43,6 +43,27 @@ __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_to_mont(ToMontArgs 
   }
 }
 
+// Montgomery digit form -> plain words
+struct FromMontArgs { ModDev mod; const uint32_t* dig; long count; uint32_t* words; int w; };
+
+template <int LPT, int TPI>
+__global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_from_mont(FromMontArgs A) {
+  HB_GROUP_PROLOGUE(LPT, TPI)
+  M mt;
+  mt.init(A.mod.n, A.mod.np);
+  const long ntiles = (A.count + IPW - 1) / IPW;
+  for (long tile = wg; tile < ntiles; tile += nw) {
+    long inst = tile * IPW + g;
+    bool valid = inst < A.count;
+    long ii = valid ? inst : A.count - 1;
+    uint32_t x[LPT], y[LPT];
+    mt.load_limbs(x, A.dig + ii * L);
+    mt.set_one(y);
+    mt.mul(x, x, y);
+    mt.store_words(A.words + ii * A.w, A.w, x, valid);
+  }
+}
+
 // ------------------------------------------------------------------------------------------------
 // Batch inversion tree.  up: dst[j] = src[2j] * src[2j+1] (copy when there is no sibling).
 struct PairUpArgs { ModDev mod; const uint32_t* src; long nsrc; uint32_t* dst; };
@@ -403,6 +424,7 @@ __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_powvar(PowVarArgs A
 struct ProductArgs {
   ModDev mod;
   const uint32_t* c; int wc;
+  int win;                  // words per INPUT element (wc, or wn when multiplying plaintext-width values)
   long ngroups, glen, gstride, estride;
   long parts, clen;
   uint32_t* out;
@@ -441,7 +463,7 @@ __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_product_pass(Produc
 #pragma unroll 1
     for (long i = 0; i < A.clen; i++) {
       long t = t0 + i;
-      if (t < A.glen) mt.load_words(y, A.c + (grp * A.gstride + t * A.estride) * A.wc, A.wc);
+      if (t < A.glen) mt.load_words(y, A.c + (grp * A.gstride + t * A.estride) * A.win, A.win);
       else mt.set_one(y);
       if (first) {
 #pragma unroll

@@ -1,0 +1,82 @@
+// C ABI, host-only translation unit: the obfuscation-factor stream.
+//
+// The reference draws r = rng.randrange(1, n) per element from a Python random.Random
+// (/root/reference/pkg/src/hebatch/paillier.py:173-178, operators.py:133,142), 23 us per element in Python at
+// 2048 bits -- slower than the modular exponentiation on the GPU.  This reproduces CPython's stream bit for bit
+// from the generator's exported state: MT19937, getrandbits(k) = little-endian 32-bit outputs with the top word
+// shifted right, randrange(1, n) = 1 + rejection sampling of getrandbits((n-1).bit_length()) below n - 1.
+// The gcd(r, n) = 1 test of draw_unit is done by the caller on the whole batch (one product on the GPU, one gcd).
+#include "hb_ctx.h"
+
+namespace {
+
+struct MT {
+  uint32_t* s;
+  int idx;
+  void refill() {
+    constexpr int N = 624, M = 397;
+    constexpr uint32_t UP = 0x80000000u, LO = 0x7fffffffu, A = 0x9908b0dfu;
+    for (int k = 0; k < N; k++) {
+      uint32_t y = (s[k] & UP) | (s[(k + 1) % N] & LO);
+      s[k] = s[(k + M) % N] ^ (y >> 1) ^ ((y & 1u) ? A : 0u);
+    }
+    idx = 0;
+  }
+  uint32_t next() {
+    if (idx >= 624) refill();
+    uint32_t y = s[idx++];
+    y ^= y >> 11;
+    y ^= (y << 7) & 0x9d2c5680u;
+    y ^= (y << 15) & 0xefc60000u;
+    y ^= y >> 18;
+    return y;
+  }
+};
+
+}  // namespace
+
+extern "C" int hb_mt19937_randrange1(uint32_t* state, int* index, const uint32_t* n_words, int wn, int64_t count,
+                                     uint32_t* out) {
+  if (!state || !index || !n_words || !out || wn <= 0 || count < 0) return hbi::fail(HB_ERR_ARG, "null pointer");
+  // bound = n - 1
+  std::vector<uint32_t> bound(n_words, n_words + wn);
+  {
+    int i = 0;
+    while (i < wn && bound[i] == 0) bound[i++] = 0xffffffffu;
+    if (i == wn) return hbi::fail(HB_ERR_ARG, "modulus is zero");
+    bound[i] -= 1;
+  }
+  int top = wn - 1;
+  while (top >= 0 && bound[top] == 0) top--;
+  if (top < 0) return hbi::fail(HB_ERR_ARG, "randrange(1, 1) is empty");
+  const int k = top * 32 + (32 - __builtin_clz(bound[top]));     // (n - 1).bit_length()
+  const int words = (k + 31) / 32;
+  MT mt{state, *index};
+  std::vector<uint32_t> cand(wn, 0);
+  for (int64_t e = 0; e < count; e++) {
+    while (true) {
+      int left = k;
+      for (int i = 0; i < words; i++, left -= 32) {
+        uint32_t r = mt.next();
+        if (left < 32) r >>= (32 - left);
+        cand[i] = r;
+      }
+      // accept when cand < bound
+      bool below = false;
+      for (int i = words - 1; i >= 0; i--) {
+        if (cand[i] != bound[i]) { below = cand[i] < bound[i]; break; }
+      }
+      if (below) break;
+    }
+    uint32_t* o = out + e * wn;
+    uint32_t carry = 1;
+    for (int i = 0; i < wn; i++) {
+      uint32_t v = (i < words ? cand[i] : 0u);
+      uint32_t s = v + carry;
+      carry = (s < v) ? 1u : 0u;
+      o[i] = s;
+    }
+  }
+  *index = mt.idx;
+  return HB_OK;
+}

@@ -62,10 +62,10 @@ def _cuda(backend) -> CudaBackend:
     return backend
 
 
-def _draw_units(pk: PublicKey, count: int, rng: random.Random) -> WordArray:
+def _draw_units(pk: PublicKey, count: int, rng: random.Random, backend: CudaBackend) -> WordArray:
     """Obfuscation factors in element order, exactly the stream draw_unit would yield
-    (operators.py:133,142)."""
-    return WordArray.from_ints([draw_unit(pk.n, rng) for _ in range(count)], pt_width(pk))
+    (operators.py:133,142) -- see CudaBackend.draw_units."""
+    return backend.draw_units(pk.n, count, rng)
 
 
 # ---- codec ------------------------------------------------------------------------------------------
@@ -94,16 +94,18 @@ def batch_encrypt(pk: PublicKey, plain: PlaintextBatch, rng: random.Random,
     """operators.py:124-136: one independent obfuscation factor per element, drawn before dispatch."""
     if plain.key != pk:
         raise ValueError("plaintext batch was encoded under a different key")
-    r = _draw_units(pk, plain.count, rng)
-    out = _cuda(backend).encrypt(pk.n, plain.words, r) if plain.count else WordArray.from_ints((), ct_width(pk))
+    be = _cuda(backend)
+    r = _draw_units(pk, plain.count, rng, be)
+    out = be.encrypt(pk.n, plain.words, r) if plain.count else WordArray.from_ints((), ct_width(pk))
     return CiphertextBatch(pk, plain.shape, plain.exponents, out, plain.shared_exponent, obfuscated=True)
 
 
 def batch_obfuscate(pk: PublicKey, cipher: CiphertextBatch, rng: random.Random,
                     backend: ExecutionBackend | None = None) -> CiphertextBatch:
     """operators.py:139-145."""
-    r = _draw_units(pk, cipher.count, rng)
-    out = _cuda(backend).obfuscate(pk.n, cipher.words, r) if cipher.count else cipher.words
+    be = _cuda(backend)
+    r = _draw_units(pk, cipher.count, rng, be)
+    out = be.obfuscate(pk.n, cipher.words, r) if cipher.count else cipher.words
     return CiphertextBatch(pk, cipher.shape, cipher.exponents, out, cipher.shared_exponent, obfuscated=True)
 
 

@@ -370,3 +370,23 @@ def test_empty_batches(okeys):
     assert ops.batch_decrypt(sk, enc).mantissas == ()
     assert ops.batch_sum(pk, enc).payload == (1,)
     assert ops.batch_add(pk, enc, enc).payload == ()
+
+
+def test_native_unit_stream_matches_python(okeys):
+    """The native MT19937 replay yields draw_unit's values and leaves the generator where Python would
+    (paillier.py:173-178); generators that are not plain random.Random take the per-element path."""
+    ok = okeys("k1024")
+    pk, _ = product_keys(ok)
+    be = CudaBackend()
+    a, b = random.Random(99), random.Random(99)
+    got = be.draw_units(pk.n, 300, a).ints()
+    assert list(got) == [ho.draw_unit(ok.n, b) for _ in range(300)]
+    assert a.getstate() == b.getstate() and a.random() == b.random()
+    # a second call continues the same stream
+    assert list(be.draw_units(pk.n, 5, a).ints()) == [ho.draw_unit(ok.n, b) for _ in range(5)]
+    seq = SequenceRng([7, 11, 13, 17])
+    assert be.draw_units(pk.n, 4, seq).ints() == (7, 11, 13, 17)
+    tiny = okeys("tiny")
+    c, d = random.Random(3), random.Random(3)
+    assert list(be.draw_units(35, 40, c).ints()) == [ho.draw_unit(35, d) for _ in range(40)]
+    assert c.getstate() == d.getstate()
