@@ -297,13 +297,26 @@ def run_b200(args):
         xk = torch.empty((inner * d, wn), dtype=torch.int32, device="cuda")
         _native.check(lib.hb_encode_f64(ctx.handle, xg.data_ptr(), -13, xk.data_ptr(), inner * d, bad.data_ptr(), stream))
         mv = torch.empty((d, wc), dtype=torch.int32, device="cuda")
-        _native.check(lib.hb_matvec(ctx.handle, c.data_ptr(), xk.data_ptr(), mv.data_ptr(), 1, inner, d, stream))
+        ab = torch.empty((2 * d, wc), dtype=torch.int32, device="cuda")
+
+        def matvec_once():
+            if world == 1:
+                _native.check(lib.hb_matvec(ctx.handle, c.data_ptr(), xk.data_ptr(), mv.data_ptr(), 1, inner, d, stream))
+                return
+            # rows are sharded: per-rank partial pairs, NCCL all-gather (d x 2 ciphertexts per rank), combine
+            _native.check(lib.hb_matvec_partial(ctx.handle, c.data_ptr(), xk.data_ptr(), ab.data_ptr(), inner, d, stream))
+            parts = [torch.empty_like(ab) for _ in range(world)]
+            dist.all_gather(parts, ab)
+            allab = torch.cat(parts, dim=0).contiguous()
+            _native.check(lib.hb_matvec_combine(ctx.handle, allab.data_ptr(), world, mv.data_ptr(), d, stream))
+
+        matvec_once()
         barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         reps = 2
         for _ in range(reps):
-            _native.check(lib.hb_matvec(ctx.handle, c.data_ptr(), xk.data_ptr(), mv.data_ptr(), 1, inner, d, stream))
+            matvec_once()
         b.record()
         barrier()
         mv_ms = a.elapsed_time(b) / reps

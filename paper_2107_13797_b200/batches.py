@@ -158,27 +158,31 @@ class CiphertextBatch(_Batch):
 # ---- plaintext-side helpers ---------------------------------------------------------------------------
 
 def _flatten(values):
+    """(flat float64 numpy array, inferred shape); nested sequences and 1-D / 2-D numpy arrays are accepted."""
+    import numpy as np
+    if isinstance(values, np.ndarray):
+        if values.ndim not in (1, 2):
+            raise ShapeMismatch(f"bad shape {values.shape}")
+        return np.ascontiguousarray(values, dtype=np.float64).ravel(), tuple(values.shape)
     values = list(values)
-    if values and isinstance(values[0], (list, tuple)):
+    if values and isinstance(values[0], (list, tuple, np.ndarray)):
         width = len(values[0])
-        flat = []
         for row in values:
             if len(row) != width:
                 raise ShapeMismatch("ragged rows")
-            flat.extend(float(v) for v in row)
-        return flat, (len(values), width)
-    return [float(v) for v in values], (len(values),)
+        return np.asarray(values, dtype=np.float64).ravel(), (len(values), width)
+    return np.asarray([float(v) for v in values], dtype=np.float64), (len(values),)
 
 
 def encode_batch(pk: PublicKey, values, shape=None, target_exponent: int | None = None) -> PlaintextBatch:
-    """Encode a flat or nested sequence under one shared exponent (batches.py:112-125): the minimum of
-    the exact exponents unless a target is given.  The mantissas are produced by the GPU codec."""
+    """Encode a flat or nested sequence (or a numpy array) under one shared exponent (batches.py:112-125): the
+    minimum of the exact exponents unless a target is given.  The mantissas are produced by the GPU codec."""
     from . import operators
     flat, inferred = _flatten(values)
     if shape is None:
         shape = inferred
     if target_exponent is None:
-        target_exponent = min((encoding.exact_exponent(v) for v in flat), default=0)
+        target_exponent = int(encoding.exact_exponents(flat).min()) if flat.size else 0
     plain = operators.batch_encode(pk, flat, target_exponent)
     return PlaintextBatch(pk, tuple(shape), (target_exponent,), plain.words, True)
 

@@ -22,7 +22,7 @@ int encrypt_common(hb_ctx* ctx, const uint32_t* m, const uint32_t* c, const uint
   CU(cudaSetDevice(ctx->device));
   const int cfg = ctx->cfg_pub;
   Launch l = plan(ctx, cfg, count);
-  const long stride = (long)(ctx->slots_n + 1) * kCfgs[cfg].lpt * 32;
+  const long stride = (long)(ctx->slots_n + 1) * kCfgs[l.cfg].lpt * 32;
   uint32_t* tbl = nullptr;
   CU(cudaMallocAsync(&tbl, (size_t)stride * l.nwarps * sizeof(uint32_t), stream));
   hb::EncArgs A;
@@ -209,7 +209,7 @@ int hb_decrypt(hb_ctx* ctx, const uint32_t* c, uint32_t* m_out, int64_t count, v
   CU(cudaSetDevice(ctx->device));
   const int cfg = ctx->cfg_priv;
   Launch l = plan(ctx, cfg, count);
-  const long stride = (long)(ctx->slots_priv + 1) * kCfgs[cfg].lpt * 32;
+  const long stride = (long)(ctx->slots_priv + 1) * kCfgs[l.cfg].lpt * 32;
   uint32_t* tbl = nullptr;
   CU(cudaMallocAsync(&tbl, (size_t)stride * l.nwarps * sizeof(uint32_t), stream));
   const uint32_t* base = ctx->d_priv;

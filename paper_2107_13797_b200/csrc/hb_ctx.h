@@ -20,7 +20,7 @@ struct ModDev {
   uint32_t np;          // -n^-1 mod 2^32
 };
 // Resident 128-thread blocks per SM the kernels are compiled for (register budget 128 or 168).
-__host__ __device__ constexpr int blocks_per_sm(int lpt) { return lpt > 20 ? 3 : 4; }
+__host__ __device__ constexpr int blocks_per_sm(int lpt) { return lpt > 24 ? 2 : lpt > 20 ? 3 : lpt <= 8 ? 6 : 4; }
 template <int LPT>
 __device__ __forceinline__ void tile_store(uint32_t* tw, int e, const uint32_t (&x)[LPT]) {
   int lane = threadIdx.x & 31;
@@ -49,13 +49,24 @@ inline int fail(int code, const std::string& msg) { g_err = msg; return code; }
 
 // Instantiated limb configurations, ordered by limb count L = LPT * TPI (capacity 32*L bits).
 struct Cfg { int lpt, tpi; };
-static const Cfg kCfgs[] = {{8, 4}, {16, 4}, {24, 4}, {16, 8}, {24, 8}};
+// 0..4: one throughput-oriented shape per limb count L = 32, 64, 96, 128, 192 (chosen by modulus size);
+// 5..7: the same L with more lanes per number -- fewer multiplies per thread, so a launch that cannot fill the
+// machine anyway finishes sooner (kernel_cfg picks by element count).  Digit-form arrays only depend on L.
+static const Cfg kCfgs[] = {{8, 4}, {16, 4}, {24, 4}, {32, 4}, {24, 8}, {8, 8}, {16, 8}, {8, 16}};
 constexpr int kNumCfg = 5;
 
 inline int pick_cfg(int bits) {
   for (int i = 0; i < kNumCfg; i++)
     if (32 * kCfgs[i].lpt * kCfgs[i].tpi >= bits) return i;
   return -1;
+}
+inline int kernel_cfg(int base, long count) {
+  if (base == 1 && count <= 14208) return 5;              // L = 64: (8, 8)
+  if (base == 3) {
+    if (count <= 7104) return 7;                          // L = 128: (8, 16)
+    if (count <= 18944) return 6;                         //          (16, 8)
+  }
+  return base;
 }
 inline int window_for(int ebits) { return ebits >= 768 ? 5 : ebits >= 160 ? 4 : ebits >= 24 ? 3 : 2; }
 
@@ -114,8 +125,10 @@ inline hb::ModDev dev_mod(const uint32_t* base, const ModOff& m) {
   return hb::ModDev{base + m.n, base + m.r1, base + m.r2, m.np};
 }
 
-struct Launch { int blocks; int threads; size_t smem; long nwarps; };
-inline Launch plan(const hb_ctx* ctx, int cfg, long count) {
+struct Launch { int blocks; int threads; size_t smem; long nwarps; int cfg; };
+// `base` is the context's shape for the modulus; the launch uses the variant that suits `count` (l.cfg).
+inline Launch plan(const hb_ctx* ctx, int base, long count) {
+  const int cfg = kernel_cfg(base, count);
   const int tpi = kCfgs[cfg].tpi, lpt = kCfgs[cfg].lpt;
   const int ipw = 32 / tpi;
   long ntiles = (count + ipw - 1) / ipw;
@@ -129,16 +142,20 @@ inline Launch plan(const hb_ctx* ctx, int cfg, long count) {
   l.smem = 0;
   (void)ipw;
   l.nwarps = blocks * 4;
+  l.cfg = cfg;
   return l;
 }
 
 #define HB_DISPATCH(cfg, KERNEL, launch, stream, args)                                           \
-  switch (cfg) {                                                                                 \
+  switch (launch.cfg) {                                                                                 \
     case 0: hb::KERNEL<8, 4><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break;  \
     case 1: hb::KERNEL<16, 4><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break; \
     case 2: hb::KERNEL<24, 4><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break; \
-    case 3: hb::KERNEL<16, 8><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break; \
+    case 3: hb::KERNEL<32, 4><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break; \
     case 4: hb::KERNEL<24, 8><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break; \
+    case 5: hb::KERNEL<8, 8><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break;  \
+    case 6: hb::KERNEL<16, 8><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break; \
+    case 7: hb::KERNEL<8, 16><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break; \
     default: return hbi::fail(HB_ERR_UNSUPPORTED, "no limb configuration");                            \
   }                                                                                              \
   hbi::g_launches++;

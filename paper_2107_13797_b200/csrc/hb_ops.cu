@@ -29,8 +29,11 @@ inline int Ldig(int cfg) { return kCfgs[cfg].lpt * kCfgs[cfg].tpi; }
     case 0: hb::KERNEL<8, 4><<<1, 32, 0, stream>>>(args); break;                     \
     case 1: hb::KERNEL<16, 4><<<1, 32, 0, stream>>>(args); break;                    \
     case 2: hb::KERNEL<24, 4><<<1, 32, 0, stream>>>(args); break;                    \
-    case 3: hb::KERNEL<16, 8><<<1, 32, 0, stream>>>(args); break;                    \
+    case 3: hb::KERNEL<32, 4><<<1, 32, 0, stream>>>(args); break;                    \
     case 4: hb::KERNEL<24, 8><<<1, 32, 0, stream>>>(args); break;                    \
+    case 5: hb::KERNEL<8, 8><<<1, 32, 0, stream>>>(args); break;                     \
+    case 6: hb::KERNEL<16, 8><<<1, 32, 0, stream>>>(args); break;                    \
+    case 7: hb::KERNEL<8, 16><<<1, 32, 0, stream>>>(args); break;                    \
     default: return hbi::fail(HB_ERR_UNSUPPORTED, "no limb configuration");          \
   }                                                                                  \
   hbi::g_launches++;
@@ -72,7 +75,7 @@ int invert_batch(hb_ctx* ctx, const uint32_t* val, long count, uint32_t* inv, Sc
   CU(cudaMemsetAsync(status, 0, sizeof(int), stream));
   {
     hb::RootInvArgs A{mod, root, words, ctx->d_pub + ctx->off_n2words, status};
-    HB_DISPATCH1(cfg, k_root_inverse, stream, A)
+    HB_DISPATCH1(kernel_cfg(cfg, 1), k_root_inverse, stream, A)
   }
   int hstatus = 0;
   CU(cudaMemcpyAsync(&hstatus, status, sizeof(int), cudaMemcpyDeviceToHost, stream));
@@ -140,7 +143,7 @@ int powscalar_impl(hb_ctx* ctx, const uint32_t* c, long ncipher, long c_div, con
   const int win = pow_window(pr.maxbits);
   const int ebits = std::max(win, (pr.maxbits + win - 1) / win * win);
   Launch l = plan(ctx, cfg, count);
-  const long stride = (long)(1 << win) * kCfgs[cfg].lpt * 32;
+  const long stride = (long)(1 << win) * kCfgs[l.cfg].lpt * 32;
   uint32_t* tbl = nullptr;
   CU(sc.get(&tbl, (size_t)stride * l.nwarps));
   hb::PowVarArgs A;

@@ -24,7 +24,7 @@ from . import encoding, operators
 from .arena import Arena, TransferLedger
 from .backends import default_backend
 from .batches import PlaintextBatch, decode_batch, encode_batch
-from .bufferpool import MiniBatchAggregator, deserialize, serialize_to_bytes
+from .bufferpool import deserialize, serialize_to_bytes
 from .paillier import KeyPair, default_rng
 
 LOGIT_EXPONENT_CAP = -8       # parties.py:39
@@ -88,11 +88,13 @@ def make_minibatches(n_rows: int, batch_size: int, seed: int):
 
 def protocol_exponent(values, cap: int = LOGIT_EXPONENT_CAP) -> int:
     """Exact shared exponent of the values, never coarser than the cap (parties.py:91-96)."""
-    return min(min((encoding.exact_exponent(float(v)) for v in values), default=0), cap)
+    values = np.asarray(values, dtype=np.float64)
+    exact = int(encoding.exact_exponents(values).min()) if values.size else 0
+    return min(exact, cap)
 
 
 def _encode(pk, values, exponent) -> PlaintextBatch:
-    return encode_batch(pk, [float(v) for v in values], target_exponent=exponent)
+    return encode_batch(pk, np.asarray(values, dtype=np.float64), target_exponent=exponent)
 
 
 class HeteroFederation:
@@ -118,8 +120,7 @@ class HeteroFederation:
         self.host_X = host_data.X.copy()
         self.guest_theta = np.zeros(self.guest_X.shape[1])
         self.host_theta = np.zeros(self.host_X.shape[1])
-        self._guest_features = MiniBatchAggregator(self.pk)
-        self._host_features = MiniBatchAggregator(self.pk)
+        self._guest_features, self._host_features = {}, {}
         self.decrypted = []          # what the arbiter saw, in order (masked gradients, loss sums)
 
     @property
@@ -144,9 +145,13 @@ class HeteroFederation:
         self.decrypted.append(values)
         return np.asarray(values)
 
-    def _features(self, aggregator, X, batch_id, idx):
-        rows = [(int(i), X[i].tolist(), None) for i in idx]
-        return aggregator.aggregate(batch_id, rows).features
+    def _features(self, cache, X, batch_id, idx):
+        """The mini-batch's feature matrix, encoded once and kept device-resident for later epochs (the role of
+        MiniBatchAggregator, bufferpool.py:182-226, without building per-row Python lists)."""
+        hit = cache.get(batch_id)
+        if hit is None:
+            hit = cache[batch_id] = encode_batch(self.pk, X[idx])
+        return hit
 
     # ---- one mini-batch (parties.py:330-340) -------------------------------------------------------------
     def step(self, batch_id: int, idx: np.ndarray):

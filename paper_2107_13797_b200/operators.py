@@ -72,7 +72,8 @@ def _draw_units(pk: PublicKey, count: int, rng: random.Random, backend: CudaBack
 
 def batch_encode(pk: PublicKey, values, exponent: int, backend: ExecutionBackend | None = None) -> PlaintextBatch:
     """operators.py:109-114."""
-    vals = np.asarray(list(values), dtype=np.float64)
+    vals = values if isinstance(values, np.ndarray) else np.asarray(list(values), dtype=np.float64)
+    vals = np.ascontiguousarray(vals, dtype=np.float64).ravel()
     if vals.shape[0] == 0:
         return PlaintextBatch(pk, (0,), (exponent,), (), True)
     words = _cuda(backend).encode_f64(pk.n, vals, exponent)
