@@ -1,0 +1,125 @@
+// Pipe-concurrency probe (B200, sm_100a): does the FP64 pipe give usable multiply throughput next to the
+// integer multiplier, and do the two issue concurrently?
+//
+//   dfma        : independent DFMA chains (multiplier changes every iteration)
+//   imad        : IMAD.WIDE.U32.X carry chains (the form mont32.cuh issues)
+//   mix_warp    : both in the same thread, interleaved
+//   mix_split   : even warps run the IMAD loop, odd warps the DFMA loop
+// Prints one JSON line with ops/s and per-SM-per-clock figures at the max clock.
+#include <cstdio>
+#include <cstdint>
+#include <cstdlib>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { \
+  fprintf(stderr, "CUDA error %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__); exit(1);} } while (0)
+
+constexpr int ND = 16;             // DFMA chains per thread
+constexpr int CH = 2, CL = 8;      // IMAD carry chains per thread
+
+__device__ __forceinline__ void dfma_step(double (&acc)[ND], const double (&a)[ND], double b) {
+#pragma unroll
+  for (int i = 0; i < ND; i++) acc[i] = __fma_rz(a[i], b, acc[i]);
+}
+
+__device__ __forceinline__ void imad_step(uint64_t (&acc)[CH * CL], const uint32_t (&a)[CL], uint32_t (&cy)[CH], uint32_t b) {
+#pragma unroll
+  for (int c = 0; c < CH; c++) {
+    uint64_t* A = acc + c * CL;
+    asm volatile(
+      "{\n\t.reg .u64 t0,t1,t2,t3,t4,t5,t6,t7;\n\t"
+      "mul.wide.u32 t0, %9, %17;\n\t mul.wide.u32 t1, %10, %17;\n\t"
+      "mul.wide.u32 t2, %11, %17;\n\t mul.wide.u32 t3, %12, %17;\n\t"
+      "mul.wide.u32 t4, %13, %17;\n\t mul.wide.u32 t5, %14, %17;\n\t"
+      "mul.wide.u32 t6, %15, %17;\n\t mul.wide.u32 t7, %16, %17;\n\t"
+      "add.cc.u64 %0, %0, t0;\n\t addc.cc.u64 %1, %1, t1;\n\t"
+      "addc.cc.u64 %2, %2, t2;\n\t addc.cc.u64 %3, %3, t3;\n\t"
+      "addc.cc.u64 %4, %4, t4;\n\t addc.cc.u64 %5, %5, t5;\n\t"
+      "addc.cc.u64 %6, %6, t6;\n\t addc.cc.u64 %7, %7, t7;\n\t"
+      "addc.u32 %8, %8, 0;\n\t}"
+      : "+l"(A[0]), "+l"(A[1]), "+l"(A[2]), "+l"(A[3]), "+l"(A[4]), "+l"(A[5]), "+l"(A[6]), "+l"(A[7]), "+r"(cy[c])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(a[4]), "r"(a[5]), "r"(a[6]), "r"(a[7]), "r"(b));
+  }
+}
+
+// mode 0: dfma, 1: imad, 2: both interleaved in every thread, 3: split by warp parity
+__global__ void __launch_bounds__(256) k_probe(uint64_t* out, uint32_t seed, int iters, int mode) {
+  double dacc[ND], da[ND];
+  uint64_t acc[CH * CL];
+  uint32_t a[CL], cy[CH];
+  uint32_t b = seed ^ (threadIdx.x * 2654435761u);
+  double db = 1.0 + (double)(b & 0xffff) * 1e-9;
+#pragma unroll
+  for (int i = 0; i < ND; i++) { dacc[i] = i; da[i] = 1.0 + 1e-7 * (i + (b & 7)); }
+#pragma unroll
+  for (int i = 0; i < CH * CL; i++) acc[i] = (uint64_t)(b + i) * 0x9E3779B97F4A7C15ull;
+#pragma unroll
+  for (int i = 0; i < CL; i++) a[i] = b * (2 * i + 3) + 12345u;
+#pragma unroll
+  for (int c = 0; c < CH; c++) cy[c] = 0;
+  const bool do_d = mode == 0 || mode == 2 || (mode == 3 && ((threadIdx.x >> 5) & 1));
+  const bool do_i = mode == 1 || mode == 2 || (mode == 3 && !((threadIdx.x >> 5) & 1));
+  if (do_d && do_i) {
+    for (int it = 0; it < iters; it++) {
+      dfma_step(dacc, da, db);
+      imad_step(acc, a, cy, b);
+      b += 0x9E3779B9u; db += 1e-9;
+    }
+  } else if (do_d) {
+    for (int it = 0; it < iters; it++) { dfma_step(dacc, da, db); db += 1e-9; }
+  } else {
+    for (int it = 0; it < iters; it++) { imad_step(acc, a, cy, b); b += 0x9E3779B9u; }
+  }
+  uint64_t s = 0;
+#pragma unroll
+  for (int i = 0; i < CH * CL; i++) s ^= acc[i];
+#pragma unroll
+  for (int c = 0; c < CH; c++) s += cy[c];
+  double ds = 0;
+#pragma unroll
+  for (int i = 0; i < ND; i++) ds += dacc[i];
+  if (s == 0x1234567ull || ds == 1.2345) out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+static double run(int blocks, int threads, int iters, uint64_t* d_out, int mode) {
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
+  for (int w = 0; w < 2; w++) k_probe<<<blocks, threads>>>(d_out, 17u + w, iters, mode);
+  CK(cudaDeviceSynchronize());
+  float best = 1e30f;
+  for (int r = 0; r < 5; r++) {
+    CK(cudaEventRecord(e0));
+    k_probe<<<blocks, threads>>>(d_out, 99u + r, iters, mode);
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0; CK(cudaEventElapsedTime(&ms, e0, e1));
+    if (ms < best) best = ms;
+  }
+  return best * 1e-3;
+}
+
+int main() {
+  cudaDeviceProp prop; CK(cudaGetDeviceProperties(&prop, 0));
+  int clk_khz = 0; CK(cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0));
+  const int sms = prop.multiProcessorCount;
+  uint64_t* d_out; CK(cudaMalloc(&d_out, (size_t)sms * 8 * 256 * sizeof(uint64_t)));
+  const int blocks = sms * 4, threads = 256, iters = 4096;
+  const double thr = (double)blocks * threads * iters;
+  const double per = 1.0 / ((double)sms * clk_khz * 1e3);
+  double t0 = run(blocks, threads, iters, d_out, 0);
+  double t1 = run(blocks, threads, iters, d_out, 1);
+  double t2 = run(blocks, threads, iters, d_out, 2);
+  double t3 = run(blocks, threads, iters, d_out, 3);
+  printf("{\"gpu\": \"%s\", \"sms\": %d, \"sm_clock_max_mhz\": %d, "
+         "\"dfma_per_s\": %.4e, \"imad_wide_x_per_s\": %.4e, "
+         "\"mix_warp\": {\"dfma_per_s\": %.4e, \"imad_per_s\": %.4e}, "
+         "\"mix_split\": {\"dfma_per_s\": %.4e, \"imad_per_s\": %.4e}, "
+         "\"per_sm_clk\": {\"dfma\": %.2f, \"imad\": %.2f, \"mix_warp_dfma\": %.2f, \"mix_warp_imad\": %.2f, "
+         "\"mix_split_dfma\": %.2f, \"mix_split_imad\": %.2f}}\n",
+         prop.name, sms, clk_khz / 1000,
+         thr * ND / t0, thr * CH * CL / t1, thr * ND / t2, thr * CH * CL / t2,
+         0.5 * thr * ND / t3, 0.5 * thr * CH * CL / t3,
+         thr * ND / t0 * per, thr * CH * CL / t1 * per, thr * ND / t2 * per, thr * CH * CL / t2 * per,
+         0.5 * thr * ND / t3 * per, 0.5 * thr * CH * CL / t3 * per);
+  return 0;
+}
