@@ -72,6 +72,24 @@ int hb_mulmod(hb_ctx* ctx, const uint32_t* a, const uint32_t* b, uint32_t* out, 
 int hb_lift_mulmod(hb_ctx* ctx, const uint32_t* a, const uint32_t* m, uint32_t* out, int64_t count,
                    int m_broadcast, void* stream);
 
+/* Plaintext-side residue arithmetic mod n (batches.py:160-205 of the reference).  plain_mul: out[i] = a[i] * b[i]
+ * mod n (b_broadcast != 0 uses b[0]); plain_add: out[i] = a[i] + b[i] mod n; plain_rescale
+ * (encoding.py:104-113): the signed mantissa times 16^digits, back as a residue -- first_bad (device int64,
+ * preset by the caller to INT64_MAX) receives the smallest index in the overflow band or beyond max_int after
+ * scaling. */
+int hb_plain_mulmod(hb_ctx* ctx, const uint32_t* a, const uint32_t* b, uint32_t* out, int64_t count,
+                    int b_broadcast, void* stream);
+int hb_plain_addmod(hb_ctx* ctx, const uint32_t* a, const uint32_t* b, uint32_t* out, int64_t count, void* stream);
+int hb_plain_rescale(hb_ctx* ctx, const uint32_t* m, int digits, uint32_t* m_out, int64_t count,
+                     int64_t* first_bad, void* stream);
+
+/* Repeated squaring, out[i] = a[i]^(2^reps) mod n^2: the inner step of every modular power on this path
+ * (gmpy2.powmod at paillier.py:190,207-208 / operators.py:41,46,53-54).  Exposed so the dedicated squaring of
+ * the kernels can be checked and timed on its own.  throughput_shape != 0 forces the limb shape large batches
+ * use, whatever `count` is. */
+int hb_sqrmod(hb_ctx* ctx, const uint32_t* a, uint32_t* out, int64_t count, int reps, int throughput_shape,
+              void* stream);
+
 /* _pow_scalar / _k_mul, operators.py:59-67: out[i] = pow_scalar(c[i], k[i % k_period]) where residues
  * k > n - n/3 are negative: the base becomes c^-1 mod n^2 and the exponent n - k.  k_period = 1
  * broadcasts one scalar, = columns broadcasts a row vector over a 2-D batch, = count is element-wise.

@@ -47,6 +47,10 @@ SIGNATURES = {
     "hb_decrypt": (_int, [_vp, _vp, _vp, _i64, _vp]),
     "hb_mulmod": (_int, [_vp, _vp, _vp, _vp, _i64, _int, _vp]),
     "hb_lift_mulmod": (_int, [_vp, _vp, _vp, _vp, _i64, _int, _vp]),
+    "hb_sqrmod": (_int, [_vp, _vp, _vp, _i64, _int, _int, _vp]),
+    "hb_plain_mulmod": (_int, [_vp, _vp, _vp, _vp, _i64, _int, _vp]),
+    "hb_plain_addmod": (_int, [_vp, _vp, _vp, _vp, _i64, _vp]),
+    "hb_plain_rescale": (_int, [_vp, _vp, _int, _vp, _i64, _vp, _vp]),
     "hb_powscalar": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _int, _vp]),
     "hb_product": (_int, [_vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp]),
     "hb_unit_product": (_int, [_vp, _vp, _vp, _i64, _vp]),

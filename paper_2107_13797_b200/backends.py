@@ -88,6 +88,40 @@ class CudaBackend(ExecutionBackend):
                                            1 if broadcast_b else 0, self._stream()))
         return out
 
+    def plain_mulmod(self, n: int, a: device.WordArray, b: device.WordArray, broadcast_b: bool = False) -> device.WordArray:
+        """out[i] = a[i] * b[i] mod n on plaintext residues (batches.plain_mul)."""
+        ctx = device.context_for(n)
+        out = device.WordArray.empty_device(a.count, ctx.wn)
+        _native.check(self.lib().hb_plain_mulmod(ctx.handle, a.ptr(), b.ptr(), out.ptr(), a.count,
+                                                 1 if broadcast_b else 0, self._stream()))
+        return out
+
+    def plain_addmod(self, n: int, a: device.WordArray, b: device.WordArray) -> device.WordArray:
+        """out[i] = a[i] + b[i] mod n on plaintext residues (batches.plain_add)."""
+        ctx = device.context_for(n)
+        out = device.WordArray.empty_device(a.count, ctx.wn)
+        _native.check(self.lib().hb_plain_addmod(ctx.handle, a.ptr(), b.ptr(), out.ptr(), a.count, self._stream()))
+        return out
+
+    def plain_rescale(self, n: int, m: device.WordArray, digits: int):
+        """Signed mantissas times 16^digits, back as residues.  Returns (words, first_bad) where first_bad is the
+        smallest index whose value is in the overflow band or leaves max_int after scaling, or -1."""
+        ctx = device.context_for(n)
+        t = device.torch()
+        out = device.WordArray.empty_device(m.count, ctx.wn)
+        bad = t.full((1,), -1, dtype=t.int64, device="cuda")
+        _native.check(self.lib().hb_plain_rescale(ctx.handle, m.ptr(), int(digits), out.ptr(), m.count,
+                                                  bad.data_ptr(), self._stream()))
+        return out, int(bad.item())
+
+    def sqrmod(self, n: int, a: device.WordArray, reps: int = 1, throughput_shape: bool = False) -> device.WordArray:
+        """out[i] = a[i]^(2^reps) mod n^2 through the kernels' squaring path."""
+        ctx = device.context_for(n)
+        out = device.WordArray.empty_device(a.count, ctx.wc)
+        _native.check(self.lib().hb_sqrmod(ctx.handle, a.ptr(), out.ptr(), a.count, reps,
+                                           1 if throughput_shape else 0, self._stream()))
+        return out
+
     def lift_mulmod(self, n: int, a: device.WordArray, m: device.WordArray, broadcast_m: bool = False) -> device.WordArray:
         ctx = device.context_for(n)
         out = device.WordArray.empty_device(a.count, ctx.wc)

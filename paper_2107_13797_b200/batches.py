@@ -209,42 +209,53 @@ def shared_exponent_of(batch) -> int:
 
 
 def plain_rescale(batch: PlaintextBatch, new_exponent: int) -> PlaintextBatch:
-    """Exact re-grid of every element onto a finer shared exponent (batches.py:160-170)."""
+    """Exact re-grid of every element onto a finer shared exponent (batches.py:160-170), on the device."""
+    from .backends import default_backend
     current = shared_exponent_of(batch)
     if new_exponent == current:
         return batch
     pk = batch.key
-    out = tuple(encoding.rescale(pk, EncodedNumber(m, current), new_exponent).mantissa
-                for m in batch.mantissas)
-    return PlaintextBatch(pk, batch.shape, (new_exponent,), out, True)
+    if new_exponent > current:
+        raise ValueError("can only rescale toward a smaller exponent")
+    if batch.count == 0:
+        return PlaintextBatch(pk, batch.shape, (new_exponent,), (), True)
+    words, bad = default_backend().plain_rescale(pk.n, batch.words, current - new_exponent)
+    if bad >= 0:
+        # the reference fails on the first offending element; let the scalar codec name the error
+        encoding.rescale(pk, batch.element(bad), new_exponent)
+        raise encoding.FixedPointOverflow(f"element {bad} cannot be rescaled to exponent {new_exponent}")
+    return PlaintextBatch(pk, batch.shape, (new_exponent,), words, True)
 
 
 def plain_mul(a: PlaintextBatch, b: PlaintextBatch) -> PlaintextBatch:
     """Encoded product, element-wise or by one broadcast scalar: mantissas multiply mod n, exponents
-    add (batches.py:173-192)."""
+    add (batches.py:173-192).  The residues are multiplied on the device."""
+    from .backends import default_backend
     require_same_key(a, b)
-    pk, n = a.key, a.key.n
+    pk = a.key
     if b.count == 1:
-        bm, be = b.mantissas[0], b.exponent_at(0)
-        prod = tuple(m * bm % n for m in a.mantissas)
+        be = b.exponent_at(0)
+        prod = default_backend().plain_mulmod(pk.n, a.words, b.words, True) if a.count else a.words
         if a.shared_exponent:
             return PlaintextBatch(pk, a.shape, (a.exponents[0] + be,), prod, True)
         return PlaintextBatch(pk, a.shape, tuple(e + be for e in a.exponents), prod, False)
     if a.shape != b.shape:
         raise ShapeMismatch(f"{a.shape} vs {b.shape}")
-    prod = tuple(x * y % n for x, y in zip(a.mantissas, b.mantissas))
+    prod = default_backend().plain_mulmod(pk.n, a.words, b.words) if a.count else a.words
+    if a.shared_exponent and b.shared_exponent:
+        return PlaintextBatch(pk, a.shape, (a.exponents[0] + b.exponents[0],), prod, True)
     exps = tuple(a.exponent_at(i) + b.exponent_at(i) for i in range(a.count))
     shared = len(set(exps)) == 1
     return PlaintextBatch(pk, a.shape, exps[:1] if shared else exps, prod, shared)
 
 
 def plain_add(a: PlaintextBatch, b: PlaintextBatch) -> PlaintextBatch:
-    """Encoded sum after exact alignment to the finer exponent (batches.py:195-205)."""
+    """Encoded sum after exact alignment to the finer exponent (batches.py:195-205), on the device."""
+    from .backends import default_backend
     require_same_key(a, b)
     if a.shape != b.shape:
         raise ShapeMismatch(f"{a.shape} vs {b.shape}")
     target = min(shared_exponent_of(a), shared_exponent_of(b))
     a, b = plain_rescale(a, target), plain_rescale(b, target)
-    n = a.key.n
-    total = tuple((x + y) % n for x, y in zip(a.mantissas, b.mantissas))
+    total = default_backend().plain_addmod(a.key.n, a.words, b.words) if a.count else a.words
     return PlaintextBatch(a.key, a.shape, (target,), total, True)

@@ -34,7 +34,7 @@ int encrypt_common(hb_ctx* ctx, const uint32_t* m, const uint32_t* c, const uint
   A.tbl_stride = stride;
   A.m = m; A.c = c; A.r = r; A.out = out;
   A.count = count; A.wn = ctx->wn; A.wc = ctx->wc; A.mode = mode;
-  HB_DISPATCH(cfg, k_encrypt, l, stream, A)
+  HB_DISPATCH_POW(cfg, k_encrypt, l, stream, A)
   CU(cudaGetLastError());
   CU(cudaFreeAsync(tbl, stream));
   return HB_OK;
@@ -92,6 +92,8 @@ int hb_ctx_create(hb_ctx** out, const uint32_t* n_words, int n_nwords, int devic
   ConstBlock cb;
   ctx->mod_n2 = add_modulus(cb, ctx->n2, L);
   ctx->off_nR = cb.add(hbh::to_limbs(hbh::shl_mod(n, 32L * L, ctx->n2), L));
+  ctx->cfg_n = pick_cfg(ctx->key_bits);
+  ctx->mod_n_pub = add_modulus(cb, n, kCfgs[ctx->cfg_n].lpt * kCfgs[ctx->cfg_n].tpi);
   std::vector<uint32_t> prog = hbh::build_program(n, window_for(ctx->key_bits), &ctx->slots_n);
   ctx->nprog_n = (int)prog.size();
   ctx->off_prog_n = cb.add(prog);
@@ -200,6 +202,53 @@ int hb_lift_mulmod(hb_ctx* ctx, const uint32_t* a, const uint32_t* m, uint32_t* 
   return mulmod_common(ctx, a, m, out, count, 1, m_broadcast, stream);
 }
 
+static int plain_common(hb_ctx* ctx, const uint32_t* a, const uint32_t* b, uint32_t* out, int64_t count,
+                        int op, int bcast, void* stream_) {
+  if (!ctx || !a || !b || !out) return fail(HB_ERR_ARG, "null pointer");
+  if (count < 0) return fail(HB_ERR_ARG, "negative count");
+  if (count == 0) return HB_OK;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  CU(cudaSetDevice(ctx->device));
+  const int cfg = ctx->cfg_n;
+  Launch l = plan(ctx, cfg, count);
+  hb::PlainArgs A;
+  A.mod = dev_mod(ctx->d_pub, ctx->mod_n_pub);
+  A.a = a; A.b = b; A.out = out; A.count = count; A.w = ctx->wn; A.op = op; A.b_broadcast = bcast;
+  HB_DISPATCH(cfg, k_plainop, l, stream, A)
+  CU(cudaGetLastError());
+  return HB_OK;
+}
+
+int hb_plain_mulmod(hb_ctx* ctx, const uint32_t* a, const uint32_t* b, uint32_t* out, int64_t count,
+                    int b_broadcast, void* stream) {
+  return plain_common(ctx, a, b, out, count, 0, b_broadcast, stream);
+}
+int hb_plain_addmod(hb_ctx* ctx, const uint32_t* a, const uint32_t* b, uint32_t* out, int64_t count, void* stream) {
+  return plain_common(ctx, a, b, out, count, 1, 0, stream);
+}
+
+int hb_sqrmod(hb_ctx* ctx, const uint32_t* a, uint32_t* out, int64_t count, int reps, int throughput_shape,
+              void* stream_) {
+  if (!ctx || !a || !out) return fail(HB_ERR_ARG, "null pointer");
+  if (count < 0 || reps < 0) return fail(HB_ERR_ARG, "negative count");
+  if (count == 0) return HB_OK;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  CU(cudaSetDevice(ctx->device));
+  const int cfg = ctx->cfg_pub;
+  Launch l = plan(ctx, cfg, throughput_shape ? (int64_t)1 << 40 : count);
+  {
+    const int ipw = 32 / kCfgs[l.cfg].tpi;
+    long blocks = ((count + ipw - 1) / ipw + 3) / 4;
+    if (blocks < l.blocks) l.blocks = (int)std::max(blocks, 1L);
+  }
+  hb::SqrArgs A;
+  A.mod = dev_mod(ctx->d_pub, ctx->mod_n2);
+  A.a = a; A.out = out; A.count = count; A.wc = ctx->wc; A.reps = reps;
+  HB_DISPATCH_SQR(cfg, k_sqrmod, l, stream, A)
+  CU(cudaGetLastError());
+  return HB_OK;
+}
+
 int hb_decrypt(hb_ctx* ctx, const uint32_t* c, uint32_t* m_out, int64_t count, void* stream_) {
   if (!ctx || !c || !m_out) return fail(HB_ERR_ARG, "null pointer");
   if (!ctx->has_private) return fail(HB_ERR_NOPRIVATE, "context has no private key");
@@ -227,7 +276,7 @@ int hb_decrypt(hb_ctx* ctx, const uint32_t* c, uint32_t* m_out, int64_t count, v
   A.qR = base + ctx->off_qR;
   A.tbl = tbl; A.tbl_stride = stride; A.stash_slot = ctx->slots_priv;
   A.c = c; A.out = m_out; A.count = count; A.wn = ctx->wn; A.wc = ctx->wc;
-  HB_DISPATCH(cfg, k_decrypt, l, stream, A)
+  HB_DISPATCH_POW(cfg, k_decrypt, l, stream, A)
   CU(cudaGetLastError());
   CU(cudaFreeAsync(tbl, stream));
   return HB_OK;

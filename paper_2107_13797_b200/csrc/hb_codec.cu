@@ -152,9 +152,100 @@ __global__ void __launch_bounds__(64) k_decode_f64(CodecArgs A) {
   A.fout[e] = neg ? -val : val;
 }
 
+// Exact re-grid onto a finer exponent (encoding.py:104-113): signed mantissa times 16^digits, range-checked
+// against max_int, stored back as a residue.  first_bad receives the smallest index that is in the overflow band
+// or overflows after scaling (the host re-examines that element to raise the reference's error).
+__global__ void __launch_bounds__(64) k_plain_rescale(CodecArgs A) {
+  extern __shared__ uint32_t stage[];
+  const int wn = A.wn, pitch = wn + 1;
+  const long base = (long)blockIdx.x * blockDim.x;
+  const long nhere = min((long)blockDim.x, A.count - base);
+  for (long idx = threadIdx.x; idx < nhere * wn; idx += blockDim.x) {
+    long el = idx / wn; int w = (int)(idx - el * wn);
+    stage[el * pitch + w] = A.min[(base + el) * wn + w];
+  }
+  __syncthreads();
+  const long e = base + threadIdx.x;
+  if (e < A.count) {
+    uint32_t* my = stage + threadIdx.x * pitch;
+    int c_max = 0, c_neg = 0;
+    for (int i = wn - 1; i >= 0; i--) {
+      uint32_t v = my[i];
+      if (c_max == 0) { uint32_t b = A.maxint[i]; c_max = v > b ? 1 : (v < b ? -1 : 0); }
+      if (c_neg == 0) { uint32_t b = A.negband[i]; c_neg = v > b ? 1 : (v < b ? -1 : 0); }
+    }
+    const bool pos = c_max < 0, neg = c_neg > 0;
+    bool over = !pos && !neg;
+    if (neg) {
+      uint32_t borrow = 0;
+      for (int i = 0; i < wn; i++) {
+        unsigned long long d = (unsigned long long)A.nwords[i] - my[i] - borrow;
+        borrow = (uint32_t)(d >> 63);
+        my[i] = (uint32_t)d;
+      }
+    }
+    // |s| << (4 * digits), in place from the top down; A.exponent carries the digit count here
+    const long shift = 4L * A.exponent;
+    const int ws = (int)min((long)wn, shift >> 5), bs = (int)(shift & 31);
+    bool nonzero = false;
+    for (int i = 0; i < wn; i++) nonzero |= my[i] != 0;
+    if (nonzero && (shift >> 5) >= wn) over = true;
+    for (int i = wn - 1; i >= wn - ws - 1 && i >= 0; i--) {       // bits that leave the top
+      uint32_t v = my[i];
+      if (i > wn - ws - 1) over |= v != 0;
+      else if (bs) over |= (v >> (32 - bs)) != 0;
+    }
+    for (int i = wn - 1; i >= 0; i--) {
+      const int src = i - ws;
+      uint32_t hi = src >= 0 ? my[src] : 0u, lo = src - 1 >= 0 ? my[src - 1] : 0u;
+      my[i] = bs ? (hi << bs) | (lo >> (32 - bs)) : hi;
+    }
+    if (!over) {
+      int cmp = 0;
+      for (int i = wn - 1; i >= 0 && cmp == 0; i--) {
+        uint32_t a = my[i], b = A.maxint[i];
+        cmp = a > b ? 1 : (a < b ? -1 : 0);
+      }
+      over = cmp >= 0;
+    }
+    if (over) atomicMin(A.first_bad, (unsigned long long)e);
+    if (neg && nonzero) {
+      uint32_t borrow = 0;
+      for (int i = 0; i < wn; i++) {
+        unsigned long long d = (unsigned long long)A.nwords[i] - my[i] - borrow;
+        borrow = (uint32_t)(d >> 63);
+        my[i] = (uint32_t)d;
+      }
+    }
+  }
+  __syncthreads();
+  for (long idx = threadIdx.x; idx < nhere * wn; idx += blockDim.x) {
+    long el = idx / wn; int w = (int)(idx - el * wn);
+    A.mout[(base + el) * wn + w] = stage[el * pitch + w];
+  }
+}
+
 }  // namespace hb
 
 extern "C" {
+
+int hb_plain_rescale(hb_ctx* ctx, const uint32_t* m, int digits, uint32_t* m_out, int64_t count,
+                     int64_t* first_bad, void* stream_) {
+  if (!ctx || !m || !m_out || !first_bad) return fail(HB_ERR_ARG, "null pointer");
+  if (count < 0 || digits < 0) return fail(HB_ERR_ARG, "negative count");
+  if (count == 0) return HB_OK;
+  CU(cudaSetDevice(ctx->device));
+  hb::CodecArgs A{};
+  A.nwords = ctx->d_pub + ctx->off_nwords; A.maxint = ctx->d_pub + ctx->off_maxint;
+  A.negband = ctx->d_pub + ctx->off_negband; A.wn = ctx->wn; A.exponent = digits; A.count = count;
+  A.min = m; A.mout = m_out; A.first_bad = (unsigned long long*)first_bad;
+  const int threads = 64;
+  const size_t smem = (size_t)threads * (ctx->wn + 1) * sizeof(uint32_t);
+  hb::k_plain_rescale<<<(unsigned)((count + threads - 1) / threads), threads, smem, (cudaStream_t)stream_>>>(A);
+  g_launches++;
+  CU(cudaGetLastError());
+  return HB_OK;
+}
 
 int hb_encode_f64(hb_ctx* ctx, const double* values, int exponent, uint32_t* m_out, int64_t count,
                   int64_t* first_bad, void* stream_) {

@@ -107,6 +107,8 @@ struct hb_ctx {
   size_t off_nR = 0, off_prog_n = 0;
   size_t off_nwords = 0, off_negband = 0, off_maxint = 0, off_n2words = 0;   // n, n - n/3 (wn words); n^2 padded for k_root_inverse
   int nprog_n = 0, slots_n = 0;
+  int cfg_n = -1;              // limb shape for arithmetic mod n (plaintext side)
+  hbi::ModOff mod_n_pub;
   // private part
   bool has_private = false;
   int cfg_priv = -1;
@@ -145,6 +147,47 @@ inline Launch plan(const hb_ctx* ctx, int base, long count) {
   l.cfg = cfg;
   return l;
 }
+
+// Dynamic shared memory of the kernels that square through Mont::sqr (k_sqrmod; k_encrypt / k_decrypt under
+// -DHB_USE_SQR): 4 warps per block.
+template <int LPT, int TPI>
+constexpr size_t sqr_smem_bytes() { return (size_t)hb::Mont<LPT, TPI>::SQ_WORDS * hb::Mont<LPT, TPI>::IPW * 4 * sizeof(uint32_t); }
+
+#define HB_SQR_CASE(KERNEL, LPT_, TPI_, launch, stream, args)                                                  \
+  {                                                                                                          \
+    constexpr size_t smem_ = hbi::sqr_smem_bytes<LPT_, TPI_>();                                              \
+    if (smem_ > 48 * 1024) {                                                                                 \
+      static bool once_ = false;                                                                             \
+      if (!once_) {                                                                                          \
+        CU(cudaFuncSetAttribute(hb::KERNEL<LPT_, TPI_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_)); \
+        once_ = true;                                                                                        \
+      }                                                                                                      \
+    }                                                                                                        \
+    hb::KERNEL<LPT_, TPI_><<<launch.blocks, launch.threads, smem_, stream>>>(args);                          \
+  }                                                                                                          \
+  break;
+
+// As HB_DISPATCH, for kernels that need the squaring scratch.
+#define HB_DISPATCH_SQR(cfg, KERNEL, launch, stream, args)                                       \
+  switch (launch.cfg) {                                                                          \
+    case 0: HB_SQR_CASE(KERNEL, 8, 4, launch, stream, args)                                      \
+    case 1: HB_SQR_CASE(KERNEL, 16, 4, launch, stream, args)                                     \
+    case 2: HB_SQR_CASE(KERNEL, 24, 4, launch, stream, args)                                     \
+    case 3: HB_SQR_CASE(KERNEL, 32, 4, launch, stream, args)                                     \
+    case 4: HB_SQR_CASE(KERNEL, 24, 8, launch, stream, args)                                     \
+    case 5: HB_SQR_CASE(KERNEL, 8, 8, launch, stream, args)                                      \
+    case 6: HB_SQR_CASE(KERNEL, 16, 8, launch, stream, args)                                     \
+    case 7: HB_SQR_CASE(KERNEL, 8, 16, launch, stream, args)                                     \
+    default: return hbi::fail(HB_ERR_UNSUPPORTED, "no limb configuration");                      \
+  }                                                                                              \
+  hbi::g_launches++;
+
+// The modular-power kernels only need the scratch when they are built to square through Mont::sqr.
+#ifdef HB_USE_SQR
+#define HB_DISPATCH_POW HB_DISPATCH_SQR
+#else
+#define HB_DISPATCH_POW HB_DISPATCH
+#endif
 
 #define HB_DISPATCH(cfg, KERNEL, launch, stream, args)                                           \
   switch (launch.cfg) {                                                                                 \

@@ -20,9 +20,14 @@ namespace hb {
 enum : uint32_t { OP_SQR = 0, OP_MUL = 1, OP_LOAD = 2, OP_KEEP = 3, OP_NODST = 0xFF };
 
 // Replays an op program on x (Montgomery form in, Montgomery form out).  Single mul call site.
+// Squarings and multiplications both go through Mont::mul by default: on the B200 the dedicated squaring
+// (Mont::sqr, 19 % fewer limb products) loses to it -- 89 k against 104 k encryptions/s at 2048 bits -- because
+// its extra non-multiply instructions are not free next to a quarter-rate IMAD.WIDE.  Build
+// with -DHB_USE_SQR to route OP_SQR through Mont::sqr and OP_MUL through Mont::mul_s; `sw` is then the instance's
+// shared-memory scratch (sqr_scratch()).
 template <int LPT, int TPI>
 __device__ __forceinline__ void run_prog(const Mont<LPT, TPI>& mt, uint32_t (&x)[LPT],
-                                         const uint32_t* __restrict__ prog, int nprog, uint32_t* tw) {
+                                         const uint32_t* __restrict__ prog, int nprog, uint32_t* tw, uint32_t* sw) {
 #pragma unroll 1
   for (int i = 0; i < nprog; i++) {
     uint32_t op = prog[i];
@@ -30,16 +35,42 @@ __device__ __forceinline__ void run_prog(const Mont<LPT, TPI>& mt, uint32_t (&x)
     if (kind == OP_LOAD) {
       tile_load<LPT>(tw, src, x);
     } else if (kind != OP_KEEP) {
-      uint32_t y[LPT];
-      if (kind == OP_MUL) {
-        tile_load<LPT>(tw, src, y);
-      } else {
+#ifdef HB_USE_SQR
+      if constexpr (Mont<LPT, TPI>::HAS_SQR) {
+        if (kind == OP_MUL) {
+          uint32_t y[LPT];
+          tile_load<LPT>(tw, src, y);
+          mt.mul_s(x, x, y, sw);
+        } else {
+          mt.sqr(x, x, sw);
+        }
+      } else
+#endif
+      {
+        uint32_t y[LPT];
+        if (kind == OP_MUL) {
+          tile_load<LPT>(tw, src, y);
+        } else {
 #pragma unroll
-        for (int k = 0; k < LPT; k++) y[k] = x[k];
+          for (int k = 0; k < LPT; k++) y[k] = x[k];
+        }
+        mt.mul(x, x, y);
       }
-      mt.mul(x, x, y);
     }
     if (dst != OP_NODST) tile_store<LPT>(tw, dst, x);
+  }
+}
+
+extern __shared__ uint32_t hb_dyn_smem[];
+// Shared-memory scratch of this lane's instance for Mont::sqr (nullptr when the shape has no dedicated squaring).
+template <int LPT, int TPI>
+__device__ __forceinline__ uint32_t* sqr_scratch() {
+  using M = Mont<LPT, TPI>;
+  if constexpr (M::HAS_SQR) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    return hb_dyn_smem + warp * (M::SQ_WORDS * M::IPW) + lane / TPI;
+  } else {
+    return nullptr;
   }
 }
 
@@ -68,6 +99,7 @@ __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_encrypt(EncArgs A) 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane / TPI;
   const long wg = (long)blockIdx.x * (blockDim.x >> 5) + warp, nw = (long)gridDim.x * (blockDim.x >> 5);
   uint32_t* tw = A.tbl + wg * A.tbl_stride;
+  uint32_t* sw = sqr_scratch<LPT, TPI>();
   const long ntiles = (A.count + IPW - 1) / IPW;
   for (long tile = wg; tile < ntiles; tile += nw) {
     long inst = tile * IPW + g;
@@ -77,7 +109,7 @@ __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_encrypt(EncArgs A) 
     mt.load_words(x, A.r + ii * A.wn, A.wn);
     mt.load_limbs(y, A.mod.r2);
     mt.mul(x, x, y);                              // Mont(r)
-    run_prog<LPT, TPI>(mt, x, A.prog, A.nprog, tw);  // Mont(r^n)
+    run_prog<LPT, TPI>(mt, x, A.prog, A.nprog, tw, sw);  // Mont(r^n)
     if (A.mode == 0) {
       uint32_t z[LPT];
       mt.load_words(y, A.m + ii * A.wn, A.wn);
@@ -137,6 +169,91 @@ __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_mulmod(MulArgs A) {
   }
 }
 
+struct PlainArgs {
+  ModDev mod;             // modulus n
+  const uint32_t* a;
+  const uint32_t* b;
+  uint32_t* out;
+  long count;
+  int w;                  // words per residue
+  int op;                 // 0: a * b mod n   1: a + b mod n
+  int b_broadcast;
+};
+
+// Plaintext-side residue arithmetic mod n (batches.py:173-205 of the reference: plain_mul, plain_add).
+template <int LPT, int TPI>
+__global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_plainop(PlainArgs A) {
+  using M = Mont<LPT, TPI>;
+  constexpr int IPW = 32 / TPI;
+  M mt;
+  mt.init(A.mod.n, A.mod.np);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane / TPI;
+  const long wg = (long)blockIdx.x * (blockDim.x >> 5) + warp, nw = (long)gridDim.x * (blockDim.x >> 5);
+  const long ntiles = (A.count + IPW - 1) / IPW;
+  for (long tile = wg; tile < ntiles; tile += nw) {
+    long inst = tile * IPW + g;
+    bool valid = inst < A.count;
+    long ii = valid ? inst : A.count - 1;
+    long ib = A.b_broadcast ? 0 : ii;
+    uint32_t x[LPT], y[LPT];
+    mt.load_words(y, A.b + ib * A.w, A.w);
+    mt.load_words(x, A.a + ii * A.w, A.w);
+    if (A.op == 0) {
+      uint32_t z[LPT];
+      mt.load_limbs(z, A.mod.r2);
+      mt.mul(y, y, z);                              // Mont(b)
+      mt.mul(x, x, y);                              // a * b mod n, canonical
+    } else {
+      mt.add_mod(x, x, y);
+    }
+    mt.store_words(A.out + ii * A.w, A.w, x, valid);
+  }
+}
+
+struct SqrArgs {
+  ModDev mod;
+  const uint32_t* a;
+  uint32_t* out;
+  long count;
+  int wc;
+  int reps;               // out = a^(2^reps)
+};
+
+// out[i] = a[i]^(2^reps) mod n^2 through the squaring path of the shape (Mont::sqr where there is one).
+template <int LPT, int TPI>
+__global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_sqrmod(SqrArgs A) {
+  using M = Mont<LPT, TPI>;
+  constexpr int IPW = 32 / TPI;
+  M mt;
+  mt.init(A.mod.n, A.mod.np);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane / TPI;
+  const long wg = (long)blockIdx.x * (blockDim.x >> 5) + warp, nw = (long)gridDim.x * (blockDim.x >> 5);
+  uint32_t* sw = sqr_scratch<LPT, TPI>();
+  const long ntiles = (A.count + IPW - 1) / IPW;
+  for (long tile = wg; tile < ntiles; tile += nw) {
+    long inst = tile * IPW + g;
+    bool valid = inst < A.count;
+    long ii = valid ? inst : A.count - 1;
+    uint32_t x[LPT], y[LPT];
+    mt.load_words(x, A.a + ii * A.wc, A.wc);
+    mt.load_limbs(y, A.mod.r2);
+    mt.mul(x, x, y);
+#pragma unroll 1
+    for (int k = 0; k < A.reps; k++) {
+      if constexpr (M::HAS_SQR) {
+        mt.sqr(x, x, sw);
+      } else {
+#pragma unroll
+        for (int i = 0; i < LPT; i++) y[i] = x[i];
+        mt.mul(x, x, y);
+      }
+    }
+    mt.set_one(y);
+    mt.mul(x, x, y);
+    mt.store_words(A.out + ii * A.wc, A.wc, x, valid);
+  }
+}
+
 struct HalfDev {
   ModDev s2;                 // modulus s^2
   ModDev s1;                 // modulus s, zero-padded to the same digit count
@@ -168,6 +285,7 @@ __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_decrypt(DecArgs A) 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane / TPI;
   const long wg = (long)blockIdx.x * (blockDim.x >> 5) + warp, nw = (long)gridDim.x * (blockDim.x >> 5);
   uint32_t* tw = A.tbl + wg * A.tbl_stride;
+  uint32_t* sw = sqr_scratch<LPT, TPI>();
   const long ntiles = (A.count + IPW - 1) / IPW;
   const int wlo = A.wc / 2, whi = A.wc - wlo;
   for (long tile = wg; tile < ntiles; tile += nw) {
@@ -188,7 +306,7 @@ __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_decrypt(DecArgs A) 
       mt.load_limbs(z, H.hiR2);
       mt.mul(y, y, z);
       mt.add_mod(x, x, y);
-      run_prog<LPT, TPI>(mt, x, H.prog, H.nprog, tw);   // Mont(c^(s-1) mod s^2)
+      run_prog<LPT, TPI>(mt, x, H.prog, H.nprog, tw, sw);   // Mont(c^(s-1) mod s^2)
       mt.set_one(z);
       mt.mul(x, x, z);                              // u = c^(s-1) mod s^2
       // u == 0 happens only when s divides c (never for a real ciphertext); the reference's floor

@@ -112,10 +112,11 @@ struct Mont {
 
   // Resolves pending single-bit carries between lanes: g (0/1) leaves this lane; returns the carry that
   // leaves the top lane (same value on every lane of the group).
-  __device__ __forceinline__ uint32_t lane_carries(uint32_t (&r)[LPT], uint32_t g, uint32_t cin0 = 0u) const {
+  template <int NW>
+  __device__ __forceinline__ uint32_t lane_carries_n(uint32_t (&r)[NW], uint32_t g, uint32_t cin0 = 0u) const {
     uint32_t all = r[0];
 #pragma unroll
-    for (int i = 1; i < LPT; i++) all &= r[i];
+    for (int i = 1; i < NW; i++) all &= r[i];
     const uint32_t G = (__ballot_sync(FULLMASK, g != 0) >> gshift) & GM;
     const uint32_t P = (__ballot_sync(FULLMASK, all == 0xffffffffu) >> gshift) & GM;
     const uint64_t S = (uint64_t)P + ((uint64_t)G << 1) + cin0;   // cin0: carry into the lowest lane
@@ -123,8 +124,11 @@ struct Mont {
     const uint32_t c = (C >> t) & 1u;
     r[0] = add_cc32(r[0], c);
 #pragma unroll
-    for (int i = 1; i < LPT; i++) r[i] = addc_cc32(r[i], 0);
+    for (int i = 1; i < NW; i++) r[i] = addc_cc32(r[i], 0);
     return (uint32_t)(S >> TPI) & 1u;
+  }
+  __device__ __forceinline__ uint32_t lane_carries(uint32_t (&r)[LPT], uint32_t g, uint32_t cin0 = 0u) const {
+    return lane_carries_n<LPT>(r, g, cin0);
   }
 
   // r = a + b + cin0 as L-limb integers (cin0 enters at the lowest limb); returns the carry out of the number
@@ -236,13 +240,17 @@ struct Mont {
         for (int k = 0; k <= H; k++) E[k] = F[k];
       }
     }
+    finish(r, E, O, pend_lo, pend_hi);
+  }
+
+  // lane value = pend + sum E[i] 2^(64 i) + sum O[i] 2^(64 i + 32)  ->  LPT + 3 words w[]
+  __device__ __forceinline__ void frame_words(uint32_t (&w)[LPT + 3], uint64_t (&E)[H + 1], uint64_t (&O)[H + 1],
+                                              uint32_t pend_lo, uint32_t pend_hi) const {
     // fold the pending column back in (once per multiplication)
     E[0] = add_cc64(E[0], ((uint64_t)pend_hi << 32) | pend_lo);
 #pragma unroll
     for (int k = 1; k < H; k++) E[k] = addc_cc64(E[k], 0);
     E[H] = addc64(E[H], 0);
-    // lane value = sum E[i] 2^(64 i) + sum O[i] 2^(64 i + 32): LPT + 3 words w[]
-    uint32_t w[LPT + 3];
     w[0] = lo32(E[0]);
     w[1] = add_cc32(hi32(E[0]), lo32(O[0]));
 #pragma unroll
@@ -251,6 +259,13 @@ struct Mont {
       w[2 * i + 1] = addc_cc32(hi32(E[i]), lo32(O[i]));
     }
     w[LPT + 2] = addc32(hi32(O[H]), 0);
+  }
+
+  // distributed frame after the last row  ->  canonical r in [0, n)
+  __device__ __forceinline__ void finish(uint32_t (&r)[LPT], uint64_t (&E)[H + 1], uint64_t (&O)[H + 1],
+                                         uint32_t pend_lo, uint32_t pend_hi) const {
+    uint32_t w[LPT + 3];
+    frame_words(w, E, O, pend_lo, pend_hi);
     // the three words above the lane's top column belong to the lane above
     uint32_t u0 = __shfl_up_sync(FULLMASK, w[LPT], 1, TPI);
     uint32_t u1 = __shfl_up_sync(FULLMASK, w[LPT + 1], 1, TPI);
@@ -267,6 +282,220 @@ struct Mont {
     const uint32_t topw = __shfl_sync(FULLMASK, w[LPT], TPI - 1, TPI);
     hi |= topw;
     cond_sub(r, hi);
+  }
+
+  // ---- shared-memory staged multiplication and dedicated squaring (TPI == 4) ---------------------------------
+  //
+  // tools/mont32_sqr_model.py is the executable description of sqr().  Both routines keep their code small enough
+  // for the instruction cache by reading the row multipliers from shared memory instead of register-indexed
+  // shuffles, which lets the row loops run at an unroll of RU instead of LPT.
+  //
+  // a^2 = sum_t a_t^2 B^(2 LPT t) + 2 sum_{i<j} a_i a_j B^(LPT (i+j)).  Every lane multiplies lane-locally
+  // (operand scanning in its own E/O frame, one column retiring per row): first its own square, then 1.5 LPT
+  // rows of the off-diagonal part -- the schedule that splits the six blocks evenly over the four lanes:
+  //     lane 0: a_0 x limbs [LPT, 2.5 LPT)      lane 3: a_0 x limbs [2.5 LPT, 4 LPT)
+  //     lane 1: a_3 x limbs [LPT, 2.5 LPT)      lane 2: a_2 x limbs [LPT, 2 LPT), then a_3 x limbs [2.5 LPT, 3 LPT)
+  // The pieces meet in shared memory (word w of an instance at sw[w * IPW]); lane t sums the columns
+  // [2 LPT t, 2 LPT (t+1)), doubles, adds its square, the lanes settle their carries, and the 2L-word square is
+  // Montgomery-reduced in the distributed frame of mul(), its high half entering one word per row at the top
+  // lane.  Limb products per lane: 2.5 LPT^2 + 4 LPT^2 against 8 LPT^2 in mul().
+  static constexpr bool HAS_SQR = (TPI == 4) && (LPT % 8 == 0);
+  static constexpr int IPW = 32 / TPI;
+  static constexpr int RU = (H % 8 == 0) ? 8 : 4;                  // rows per unrolled chunk (divides H)
+  static constexpr int SQ_P0 = 0, SQ_P3 = 5 * H + 1, SQ_P1 = 10 * H + 2, SQ_P2A = 15 * H + 3, SQ_P2B = 19 * H + 3;
+  static constexpr int SQ_T = 22 * H + 4;                          // 2L words: own squares, then the square
+  static constexpr int SQ_A = SQ_T + 16 * H;                       // staged operand: limb j at SQ_A + j + j / LPT
+  static constexpr int SQ_WORDS = HAS_SQR ? SQ_A + L + TPI : 0;    // shared-memory words per instance
+
+  __device__ __forceinline__ void stage(const uint32_t (&x)[LPT], uint32_t* sw) const {
+    uint32_t* d = sw + (SQ_A + (LPT + 1) * t) * IPW;
+#pragma unroll
+    for (int k = 0; k < LPT; k++) d[k * IPW] = x[k];
+  }
+
+  // the frame moves down one column; `recv` lands on the top column
+  __device__ __forceinline__ void frame_down(uint64_t (&E)[H + 1], uint64_t (&O)[H + 1], uint32_t recv) const {
+    uint64_t F[H + 1];
+#pragma unroll
+    for (int k = 0; k <= H; k++) F[k] = O[k];
+#pragma unroll
+    for (int k = 0; k < H - 1; k++) O[k] = E[k + 1];
+    O[H - 1] = add_cc64(E[H], (uint64_t)recv);
+    O[H] = addc64(0, 0);
+#pragma unroll
+    for (int k = 0; k <= H; k++) E[k] = F[k];
+  }
+
+  // mul() with b read from shared memory: same arithmetic, row loop unrolled RU times
+  __device__ __forceinline__ void mul_s(uint32_t (&r)[LPT], const uint32_t (&a)[LPT], const uint32_t (&b)[LPT],
+                                        uint32_t* sw) const {
+    uint64_t E[H + 1], O[H + 1];
+#pragma unroll
+    for (int i = 0; i <= H; i++) { E[i] = 0; O[i] = 0; }
+    uint32_t pend_lo = 0, pend_hi = 0;
+    __syncwarp();
+    stage(b, sw);
+    __syncwarp();
+#pragma unroll 1
+    for (int j0 = 0; j0 < L; j0 += RU) {
+      const uint32_t* bs = sw + (SQ_A + j0 + j0 / LPT) * IPW;
+#pragma unroll
+      for (int u = 0; u < RU; u++) {
+        mac_row(E, O, a, bs[u * IPW]);
+        uint32_t q = (lo32(E[0]) + pend_lo) * np;
+        q = __shfl_sync(FULLMASK, q, 0, TPI);
+        mac_row(E, O, n, q);
+        const uint32_t vlo = add_cc32(lo32(E[0]), pend_lo);
+        const uint32_t vhi = addc_cc32(hi32(E[0]), pend_hi);
+        const uint32_t vtop = addc32(0, 0);
+        uint32_t recv = __shfl_down_sync(FULLMASK, vlo, 1, TPI);
+        recv = top ? 0u : recv;
+        pend_lo = vhi;
+        pend_hi = vtop;
+        frame_down(E, O, recv);
+      }
+    }
+    finish(r, E, O, pend_lo, pend_hi);
+  }
+
+  // r = a * a / R mod n, canonical.  sw: this instance's shared-memory scratch (SQ_WORDS words, stride IPW).
+  __device__ __forceinline__ void sqr(uint32_t (&r)[LPT], const uint32_t (&a)[LPT], uint32_t* sw) const {
+    constexpr int W = 2 * LPT;
+    uint64_t E[H + 1], O[H + 1];
+#pragma unroll
+    for (int i = 0; i <= H; i++) { E[i] = 0; O[i] = 0; }
+    uint32_t pend_lo = 0, pend_hi = 0;
+    uint32_t v[LPT];
+    __syncwarp();
+    stage(a, sw);
+    __syncwarp();
+    // ---- lane-local products: LPT rows of the own square, LPT rows of phase alpha, LPT / 2 of phase beta
+    const int pa = t == 0 ? SQ_P0 : t == 1 ? SQ_P1 : t == 2 ? SQ_P2A : SQ_P3;
+#pragma unroll 1
+    for (int row0 = 0; row0 < 5 * H; row0 += RU) {
+      const int phase = row0 < LPT ? 0 : row0 < 2 * LPT ? 1 : 2;
+      const int pr = row0 - phase * LPT;                          // row inside the phase
+      int vsrc, x0, d0;
+      if (phase == 0) {
+        vsrc = t; x0 = LPT * t; d0 = SQ_T + W * t;
+      } else if (phase == 1) {
+        vsrc = t == 1 ? 3 : t == 2 ? 2 : 0; x0 = t == 3 ? 5 * H : LPT; d0 = pa;
+      } else {
+        vsrc = (t == 1 || t == 2) ? 3 : 0; x0 = t == 3 ? 7 * H : t == 2 ? 5 * H : 2 * LPT;
+        d0 = t == 2 ? SQ_P2B : pa + LPT;
+      }
+      if (pr == 0) {
+        const uint32_t* vs = sw + (SQ_A + (LPT + 1) * vsrc) * IPW;
+#pragma unroll
+        for (int k = 0; k < LPT; k++) v[k] = vs[k * IPW];
+      }
+      const int j0 = x0 + pr;
+      const uint32_t* xs = sw + (SQ_A + j0 + j0 / LPT) * IPW;
+      uint32_t* dst = sw + (d0 + pr) * IPW;
+#pragma unroll
+      for (int u = 0; u < RU; u++) {
+        mac_row(E, O, v, xs[u * IPW]);
+        const uint32_t vlo = add_cc32(lo32(E[0]), pend_lo);
+        const uint32_t vhi = addc_cc32(hi32(E[0]), pend_hi);
+        const uint32_t vtop = addc32(0, 0);
+        dst[u * IPW] = vlo;
+        pend_lo = vhi;
+        pend_hi = vtop;
+        frame_down(E, O, 0u);
+      }
+      const int plen = phase == 2 ? H : LPT;
+      if (pr + RU == plen && (phase != 1 || t == 2)) {            // the piece ends here: park the rest of the frame
+        uint32_t w[LPT + 3];
+        frame_words(w, E, O, pend_lo, pend_hi);
+#pragma unroll
+        for (int k = 0; k < LPT; k++) dst[(RU + k) * IPW] = w[k];
+#pragma unroll
+        for (int i = 0; i <= H; i++) { E[i] = 0; O[i] = 0; }
+        pend_lo = 0;
+        pend_hi = 0;
+      }
+    }
+    __syncwarp();
+    // ---- column sums: lane t owns the columns [W t, W (t + 1))
+    {
+      uint32_t acc[W];
+#pragma unroll
+      for (int k = 0; k < W; k++) acc[k] = 0;
+      uint32_t topc = 0;
+#pragma unroll 1
+      for (int p = 0; p < 5; p++) {
+        const int pb = p == 0 ? SQ_P0 : p == 1 ? SQ_P3 : p == 2 ? SQ_P1 : p == 3 ? SQ_P2A : SQ_P2B;
+        const int off = p == 0 ? 2 * H : p == 1 ? 5 * H : p == 2 ? 8 * H : p == 3 ? 6 * H : 11 * H;
+        const int len = p == 3 ? 4 * H : p == 4 ? 3 * H : 5 * H;
+        const int base = W * t - off;
+        if (base + W <= 0 || base >= len) continue;               // no overlap with this lane's columns
+        const uint32_t* ps = sw + (pb + base) * IPW;
+        uint32_t w[W];
+#pragma unroll
+        for (int k = 0; k < W; k++) w[k] = ((unsigned)(base + k) < (unsigned)len) ? ps[k * IPW] : 0u;
+        acc[0] = add_cc32(acc[0], w[0]);
+#pragma unroll
+        for (int k = 1; k < W; k++) acc[k] = addc_cc32(acc[k], w[k]);
+        topc = addc32(topc, 0);
+      }
+      // the off-diagonal part counts twice
+      topc = 2 * topc + (acc[W - 1] >> 31);
+#pragma unroll
+      for (int k = W - 1; k > 0; k--) acc[k] = __funnelshift_l(acc[k - 1], acc[k], 1);
+      acc[0] <<= 1;
+      uint32_t* tt = sw + (SQ_T + W * t) * IPW;
+      {
+        uint32_t w[W];
+#pragma unroll
+        for (int k = 0; k < W; k++) w[k] = tt[k * IPW];
+        acc[0] = add_cc32(acc[0], w[0]);
+#pragma unroll
+        for (int k = 1; k < W; k++) acc[k] = addc_cc32(acc[k], w[k]);
+        topc = addc32(topc, 0);
+      }
+      uint32_t in = __shfl_up_sync(FULLMASK, topc, 1, TPI);
+      if (t == 0) in = 0;
+      acc[0] = add_cc32(acc[0], in);
+#pragma unroll
+      for (int k = 1; k < W; k++) acc[k] = addc_cc32(acc[k], 0);
+      const uint32_t g = addc32(0, 0);
+      lane_carries_n<W>(acc, g);
+#pragma unroll
+      for (int k = 0; k < W; k++) tt[k * IPW] = acc[k];
+    }
+    __syncwarp();
+    // ---- Montgomery reduction of the 2L-word square
+    {
+      const uint32_t* tl = sw + (SQ_T + LPT * t) * IPW;
+#pragma unroll
+      for (int i = 0; i < H; i++) {
+        E[i] = (uint64_t)tl[(2 * i) * IPW] | ((uint64_t)tl[(2 * i + 1) * IPW] << 32);
+        O[i] = 0;
+      }
+      E[H] = 0;
+      O[H] = 0;
+      pend_lo = 0;
+      pend_hi = 0;
+    }
+#pragma unroll 1
+    for (int row = 0; row < L; row += RU) {
+      const uint32_t* th = sw + (SQ_T + L + row) * IPW;
+#pragma unroll
+      for (int u = 0; u < RU; u++) {
+        uint32_t q = (lo32(E[0]) + pend_lo) * np;
+        q = __shfl_sync(FULLMASK, q, 0, TPI);
+        mac_row(E, O, n, q);
+        const uint32_t vlo = add_cc32(lo32(E[0]), pend_lo);
+        const uint32_t vhi = addc_cc32(hi32(E[0]), pend_hi);
+        const uint32_t vtop = addc32(0, 0);
+        uint32_t recv = __shfl_down_sync(FULLMASK, vlo, 1, TPI);
+        if (top) recv = th[u * IPW];
+        pend_lo = vhi;
+        pend_hi = vtop;
+        frame_down(E, O, recv);
+      }
+    }
+    finish(r, E, O, pend_lo, pend_hi);
   }
 
   // limbs [t*LPT, (t+1)*LPT) of the little-endian word array w[0..nwords) (zero beyond it)

@@ -390,3 +390,86 @@ def test_native_unit_stream_matches_python(okeys):
     c, d = random.Random(3), random.Random(3)
     assert list(be.draw_units(35, 40, c).ints()) == [ho.draw_unit(35, d) for _ in range(40)]
     assert c.getstate() == d.getstate()
+
+
+# ---- plaintext-side residue algebra on the device (reference batches.py:160-205, encoding.py:104-113) -------
+
+def test_plain_algebra_small(okeys):
+    from paper_2107_13797_b200.batches import plain_add, plain_mul, plain_rescale
+    ok = okeys("k128")
+    pk = paillier.PublicKey(ok.n)
+    a = PlaintextBatch(pk, (3,), (-2,), (5, ok.n - 7, 0), True)
+    b = PlaintextBatch(pk, (3,), (-1,), (2, 3, ok.n - 1), True)
+    r = plain_rescale(b, -2)
+    assert r.mantissas == (32, 48, ok.n - 16) and r.exponents == (-2,)
+    s = plain_add(a, b)
+    assert s.mantissas == (37, 41, ok.n - 16) and s.exponents == (-2,)
+    m = plain_mul(a, b)
+    assert m.mantissas == (10, (ok.n - 21), 0) and m.exponents == (-3,) and m.shared_exponent
+    k = PlaintextBatch(pk, (1,), (-1,), (4,), True)
+    assert plain_mul(a, k).mantissas == (20, ok.n - 28, 0)
+    with pytest.raises(ShapeMismatch):
+        plain_add(a, PlaintextBatch(pk, (2,), (0,), (1, 2), True))
+    with pytest.raises(ValueError):
+        plain_rescale(a, -1)
+
+
+@pytest.mark.parametrize("name", KEYS)
+def test_plain_algebra_matches_oracle(okeys, name):
+    from paper_2107_13797_b200.batches import plain_add, plain_mul, plain_rescale
+    ok = okeys(name)
+    pk = paillier.PublicKey(ok.n)
+    rng = random.Random(sum(map(ord, name)))
+    count = 67
+    n, max_int = ok.n, ok.n // 3
+    xs = [rng.randrange(n) for _ in range(count)]
+    ys = [rng.randrange(n) for _ in range(count)]
+    xs[:4] = [0, 1, n - 1, n // 2]
+    ys[:4] = [n - 1, n - 1, n - 1, 2]
+    a = PlaintextBatch(pk, (count,), (-3,), tuple(xs), True)
+    b = PlaintextBatch(pk, (count,), (-5,), tuple(ys), True)
+    prod = plain_mul(a, b)
+    assert prod.mantissas == tuple(x * y % n for x, y in zip(xs, ys)) and prod.exponents == (-8,)
+    k = PlaintextBatch(pk, (1,), (-1,), (ys[5],), True)
+    assert plain_mul(a, k).mantissas == tuple(x * ys[5] % n for x in xs)
+    same = PlaintextBatch(pk, (count,), (-3,), tuple(ys), True)
+    assert plain_add(a, same).mantissas == tuple((x + y) % n for x, y in zip(xs, ys))
+    # rescale: small signed magnitudes (what the protocols hold), every shift 0..40 digits that still fits
+    bits = max(2, max_int.bit_length() - 1)
+    for digits in (1, 2, 7, 8, 9, 16, 33):
+        room = bits - 4 * digits
+        if room < 2:
+            continue
+        mags = [rng.getrandbits(rng.randrange(1, room)) for _ in range(count)]
+        mags[0], mags[1] = 0, (1 << (room - 1)) - 1
+        res = [m if rng.random() < 0.5 else (n - m) % n for m in mags]
+        pb = PlaintextBatch(pk, (count,), (-2,), tuple(res), True)
+        got = plain_rescale(pb, -2 - digits)
+        assert got.mantissas == tuple(ho.rescale(ok, m, -2, -2 - digits) for m in res), (name, digits)
+        assert got.exponents == (-2 - digits,)
+
+
+def test_plain_rescale_overflow(okeys):
+    from paper_2107_13797_b200.batches import plain_rescale
+    from paper_2107_13797_b200.encoding import FixedPointOverflow
+    for name in ("tiny", "k128", "k1024"):
+        ok = okeys(name)
+        pk = paillier.PublicKey(ok.n)
+        n, max_int = ok.n, ok.n // 3
+        # scaled magnitude reaches max_int
+        big = max_int // 16 + 1
+        for bad in (big, n - big):
+            pb = PlaintextBatch(pk, (3,), (0,), (1, bad, 2), True)
+            with pytest.raises(FixedPointOverflow):
+                plain_rescale(pb, -1)
+            with pytest.raises(ho.Overflow):
+                ho.rescale(ok, bad, 0, -1)
+        # a residue inside the overflow band cannot be interpreted at all
+        pb = PlaintextBatch(pk, (2,), (0,), (1, max_int + 1), True)
+        with pytest.raises(FixedPointOverflow):
+            plain_rescale(pb, -1)
+        # the largest magnitudes that still fit do
+        fit = (max_int - 1) // 16
+        if fit:
+            ok_batch = PlaintextBatch(pk, (2,), (0,), (fit, n - fit), True)
+            assert plain_rescale(ok_batch, -1).mantissas == (fit * 16, n - fit * 16)

@@ -107,23 +107,6 @@ def test_batch_value_semantics():
     assert words_to_ints(ints_to_words([2 ** 70 + 3, 0], 3)) == (2 ** 70 + 3, 0)
 
 
-def test_plain_algebra():
-    ok = ho.keygen(128, random.Random(1234))
-    pk = paillier.PublicKey(ok.n)
-    a = PlaintextBatch(pk, (3,), (-2,), (5, ok.n - 7, 0), True)
-    b = PlaintextBatch(pk, (3,), (-1,), (2, 3, ok.n - 1), True)
-    r = plain_rescale(b, -2)
-    assert r.mantissas == (32, 48, ok.n - 16) and r.exponents == (-2,)
-    s = plain_add(a, b)
-    assert s.mantissas == (37, 41, ok.n - 16) and s.exponents == (-2,)
-    m = plain_mul(a, b)
-    assert m.mantissas == (10, (ok.n - 21), 0) and m.exponents == (-3,) and m.shared_exponent
-    k = PlaintextBatch(pk, (1,), (-1,), (4,), True)
-    assert plain_mul(a, k).mantissas == (20, ok.n - 28, 0)
-    with pytest.raises(ShapeMismatch):
-        plain_add(a, PlaintextBatch(pk, (2,), (0,), (1, 2), True))
-
-
 def test_backend_registry():
     with pytest.raises(ValueError):
         get_backend("naive")
