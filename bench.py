@@ -47,6 +47,9 @@ def parse_args():
     ap.add_argument("--cpu-sample", type=int, default=4096, help="elements of the bounded CPU sample")
     ap.add_argument("--no-matvec", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-flr", action="store_true")
+    ap.add_argument("--flr-rows", type=int, default=50_000,
+                    help="rows of the heterogeneous-FLR extra (BASELINE configs[3] shape, 200 features)")
     return ap.parse_args()
 
 
@@ -330,6 +333,10 @@ def run_b200(args):
         # canonical work: (1.25 * 52 + 1) modmuls per term (SURVEY.md 8d, 52-bit scalars)
         extras["matvec_canonical_lp_per_s"] = terms * (1.25 * 52 + 1) * LP_MODMUL / (mv_ms * 1e-3)
 
+    # ---- extra: one full-batch iteration of heterogeneous FLR (BASELINE configs[3] shape at reduced rows)
+    if not args.no_flr and world == 1 and count >= 100_000:
+        extras.update(flr_extra(args.flr_rows))
+
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
@@ -339,7 +346,7 @@ def run_b200(args):
     enc_s = enc_ms * 1e-3 / args.steps            # average k_encrypt launch duration (one launch per step)
     achieved = LP_ENCRYPT * count / enc_s
     roofline = {
-        "bound": "imad", "kernel": "k_encrypt<16,8>", "achieved": achieved / 1e12, "peak": peak / 1e12,
+        "bound": "imad", "kernel": "k_encrypt<32,4>", "achieved": achieved / 1e12, "peak": peak / 1e12,
         "unit": "TLP/s (1e12 32x32->64 limb products per second)", "frac": achieved / peak,
         "traffic": _ncu_traffic_per_element() * count if _ncu_traffic_per_element() else None,
         "peak_source": peak_src,
@@ -370,11 +377,39 @@ def run_b200(args):
         dist.destroy_process_group()
 
 
+def flr_extra(rows: int, features: int = 200):
+    """Two full-batch iterations (gradient step + loss over all rows) of 2-party heterogeneous FLR through the
+    package's operator API at Paillier-2048; the second one is reported (the first also encodes the feature
+    matrices, which stay resident).  Per iteration: 5 * rows full-width modular powers, two rows x ~100 encrypted
+    matvecs, ~3 * rows scalar powers, ~4 * rows modular products, 202 decryptions."""
+    import numpy as np
+    import torch
+    from paper_2107_13797_b200 import flr, paillier
+    ids, X, y = flr.make_synthetic(rows, features, seed=42)
+    guest, host = flr.vertical_split(ids, X, y, 2)
+    keys = paillier.keygen(KEY_BITS, paillier.default_rng(KEY_SEED), allow_insecure=True)
+    fed = flr.HeteroFederation(guest, host, [np.arange(rows)], np.arange(rows), keys,
+                               flr.FlrConfig(0.15, rows, seed=42))
+    secs, losses = [], []
+    for _ in range(2):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = fed.run_epoch()
+        torch.cuda.synchronize()
+        secs.append(time.perf_counter() - t0)
+        losses.append(res.loss)
+    if not (losses[1] < losses[0] < 0.6932):
+        raise SystemExit(f"FLR loss did not decrease: {losses}")
+    return {"flr_hetero_iter_s": secs[1], "flr_first_iter_s": secs[0], "flr_rows": rows, "flr_features": features,
+            "flr_modexp_per_iter": 5 * rows + 2 * (features + 1) + 1, "flr_loss": losses}
+
+
 def _ncu_traffic_per_element():
     """dram bytes read + written per encrypted element, from the committed ncu --set full capture of k_encrypt
-    (profiles/r01_ncu_summary.json; the capture ran 37888 elements)."""
+    (profiles/r01b_ncu_summary.json; the capture ran 37888 elements).  Almost all of it is write-back of the
+    per-warp window tables (17 slots x 4 KiB per warp), not operand traffic."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_summary.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", "r01b_ncu_summary.json")) as fh:
             enc = json.load(fh)["encrypt"]
         mb = float(enc["dram__bytes_read.sum"]["value"]) + float(enc["dram__bytes_write.sum"]["value"])
         return mb * 1e6 / 37888

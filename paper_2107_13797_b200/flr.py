@@ -1,13 +1,13 @@
-"""Heterogeneous (vertical) federated logistic regression on the B200 operators.
+"""Federated logistic regression on the B200 operators: heterogeneous (vertical) and homogeneous (horizontal).
 
 This is the caller of the hot path: the per-mini-batch message flow of the reference's
 flr/parties.py (HeteroGuest :135-225, HeteroHost :228-276, Arbiter :279-305, HeteroFederation :308-354),
 driven through this package's operators, arena and wire format.  It keeps the reference's operator
 sequence, exponent choices, random-stream layout (guest: seed*4+1, guest arena: seed*4+2, host: seed*4+3) and
 hop-by-hop serialisation, so with the same data, key and seed every ciphertext -- and therefore every
-decrypted masked gradient, the model and the loss -- equals the reference's run.  What it does not carry over is
-the reference's control plane (ChannelHub message audit, homogeneous mode, CLI): messages are passed as HAFB bytes
-between the three roles inside one object.
+decrypted masked gradient, the model and the loss -- equals the reference's run.  HomoFederation does the same for the
+horizontal mode (parties.py:357-454).  What is not carried over is the reference's control plane (ChannelHub
+message audit, CLI): messages are passed as HAFB bytes between the roles inside one object.
 
 Second-order Taylor objective (reference flr/objective.py): fore gradient 0.25 * theta.x - 0.5 * y, loss
 log 2 - 0.5 y z + 0.125 z^2 with z = theta.x.
@@ -28,6 +28,7 @@ from .bufferpool import deserialize, serialize_to_bytes
 from .paillier import KeyPair, default_rng
 
 LOGIT_EXPONENT_CAP = -8       # parties.py:39
+HOMO_GRADIENT_EXPONENT = -12  # parties.py:40
 MASK_RANGE = 8.0              # parties.py:41
 LOG2 = math.log(2.0)
 
@@ -77,6 +78,17 @@ def vertical_split(ids, X, y, parties: int = 2):
     cuts = [round(i * d / parties) for i in range(parties + 1)]
     return [PartyData("guest" if i == 0 else "host", ids, X[:, cuts[i]:cuts[i + 1]].copy(), y.copy() if i == 0 else None)
             for i in range(parties)]
+
+
+def horizontal_split(ids, X, y, parties: int):
+    """Round-robin row assignment, every party keeps all columns (flr/data.py:125-136)."""
+    if parties < 1:
+        raise ValueError("need at least one party")
+    out = []
+    for i in range(parties):
+        take = np.arange(i, len(ids), parties)
+        out.append(PartyData(f"party{i}", tuple(ids[j] for j in take), X[take].copy(), y[take].copy()))
+    return out
 
 
 def make_minibatches(n_rows: int, batch_size: int, seed: int):
@@ -233,3 +245,61 @@ class HeteroFederation:
 
     def combined_theta(self) -> np.ndarray:
         return np.concatenate([self.guest_theta, self.host_theta])
+
+
+class HomoFederation:
+    """Horizontal federation (reference flr/parties.py:357-454): every party encrypts its full-batch Taylor
+    gradient at exponent -12, the arbiter weights each vector by the party's row count (a scalar power), adds
+    them homomorphically and decrypts only the aggregate; the epoch loss travels the same way as one encrypted
+    sum per party.  Random streams as in the reference (party i: (seed + 13) * 31 + i), so with the same data, key
+    and seed the aggregated gradients, the model and the loss equal the reference's."""
+
+    def __init__(self, party_data, keys: KeyPair, config: FlrConfig, backend=None):
+        if len({p.X.shape[1] for p in party_data}) != 1:
+            raise ValueError("horizontal parties must share one feature schema")
+        self.keys = keys
+        self.pk = keys.public
+        self.config = config
+        self.backend = backend or default_backend()
+        self.parties = [{"name": p.name, "rng": default_rng((config.seed + 13) * 31 + i),
+                         "X": np.hstack([p.X, np.ones((p.rows, 1))]), "y": p.y}
+                        for i, p in enumerate(party_data)]
+        self.theta = np.zeros(self.parties[0]["X"].shape[1])
+        self.epoch = 0
+        self.aggregated_gradients = []
+
+    def _send(self, party, values) -> tuple:
+        """Encode at the protocol exponent, encrypt with the party's stream, ship as HAFB bytes."""
+        plain = _encode(self.pk, [float(v) for v in values], HOMO_GRADIENT_EXPONENT)
+        cipher = operators.batch_encrypt(self.pk, plain, party["rng"], self.backend)
+        return serialize_to_bytes(cipher), len(party["X"])
+
+    def run_epoch(self) -> EpochResult:
+        pk, be = self.pk, self.backend
+        wires = []
+        for party in self.parties:                                        # parties.py:373-381
+            X, y = party["X"], party["y"]
+            grad = (0.25 * (X @ self.theta) - 0.5 * y) @ X / len(y)
+            wires.append(self._send(party, grad))
+        total_rows = sum(rows for _, rows in wires)
+        acc = None
+        for wire, rows in wires:                                          # parties.py:422-428
+            cipher = deserialize(wire, pk)
+            weight = encode_batch(pk, [float(rows)], target_exponent=0)
+            weighted = operators.batch_mul_plain(pk, cipher, weight, be)
+            acc = weighted if acc is None else operators.batch_add(pk, acc, weighted, be)
+        aggregated = np.asarray(decode_batch(pk, operators.batch_decrypt(self.keys.private, acc, be))) / total_rows
+        self.aggregated_gradients.append(aggregated)
+        self.theta = self.theta - self.config.learning_rate * aggregated
+        loss_acc = None
+        for party in self.parties:                                        # parties.py:383-389, 439-446
+            z = party["X"] @ self.theta
+            total = float(np.sum(LOG2 - 0.5 * party["y"] * z + 0.125 * z * z))
+            cipher = deserialize(self._send(party, [total])[0], pk)
+            loss_acc = cipher if loss_acc is None else operators.batch_add(pk, loss_acc, cipher, be)
+        loss = decode_batch(pk, operators.batch_decrypt(self.keys.private, loss_acc, be))[0] / total_rows
+        self.epoch += 1
+        return EpochResult(self.epoch, loss, float(np.linalg.norm(aggregated)), TransferLedger().to_json())
+
+    def run(self, epochs: int):
+        return [self.run_epoch() for _ in range(epochs)]

@@ -42,3 +42,20 @@ def test_hetero_flr_equals_reference(name):
     assert results[-1].ledger == case["ledger"]
     assert fed.arena.check_conservation()
     print(f"{name}: {secs:.2f}s on the GPU vs {case['reference_seconds']:.2f}s reference CPU")
+
+
+@pytest.mark.parametrize("name", ["homo_1024", "homo_8party_512"])
+def test_homo_flr_equals_reference(name):
+    """Horizontal mode (BASELINE configs[4] shape, reduced): encrypted gradient vectors weighted by row count,
+    added and decrypted only in aggregate -- aggregated gradients, model and loss equal the reference's."""
+    case = GOLD[name]
+    ids, X, y = flr.make_synthetic(case["rows"], case["features"], seed=case["seed"])
+    parts = flr.horizontal_split(ids, X, y, case["parties"])
+    keys = paillier.keygen(case["key_bits"], paillier.default_rng(case["key_seed"]), allow_insecure=True)
+    assert format(keys.public.n, "x") == case["n"]
+    fed = flr.HomoFederation(parts, keys, flr.FlrConfig(learning_rate=0.15, seed=case["seed"]))
+    results = fed.run(case["epochs"])
+    assert [r.loss.hex() for r in results] == case["loss"]
+    assert [r.grad_norm.hex() for r in results] == case["grad_norm"]
+    assert [float(v).hex() for v in fed.theta] == case["theta"]
+    assert [[float(v).hex() for v in g] for g in fed.aggregated_gradients] == case["aggregated_gradients"]

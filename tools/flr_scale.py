@@ -88,11 +88,14 @@ def main():
     setup = time.perf_counter() - t0
     per_iter, losses = [], []
     prof = None
-    if args.profile:
-        import cProfile
-        prof = cProfile.Profile()
-        prof.enable()
-    for _ in range(args.iters):
+    for it in range(args.iters):
+        if it == args.iters - 1:          # the breakdown reports the last (steady-state) iteration only
+            SPENT.clear()
+            CALLS.clear()
+            if args.profile:
+                import cProfile
+                prof = cProfile.Profile()
+                prof.enable()
         t0 = time.perf_counter()
         res = fed.run_epoch()
         _sync()
@@ -107,7 +110,7 @@ def main():
         "rows": args.rows, "features": args.features, "key_bits": args.key_bits, "iters": args.iters,
         "setup_s": round(setup, 2), "s_per_iter": [round(t, 3) for t in per_iter], "loss": losses,
         "breakdown_s": {k: round(v, 3) for k, v in sorted(SPENT.items(), key=lambda kv: -kv[1])},
-        "calls": dict(CALLS), "outside_ops_s": round(sum(per_iter) - inside, 3),
+        "calls": dict(CALLS), "outside_ops_s": round(per_iter[-1] - inside, 3),
         "ledger": fed.ledger.to_json(),
     }))
 
