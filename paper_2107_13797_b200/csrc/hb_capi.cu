@@ -238,7 +238,7 @@ int hb_sqrmod(hb_ctx* ctx, const uint32_t* a, uint32_t* out, int64_t count, int 
   Launch l = plan(ctx, cfg, throughput_shape ? (int64_t)1 << 40 : count);
   {
     const int ipw = 32 / kCfgs[l.cfg].tpi;
-    long blocks = ((count + ipw - 1) / ipw + 3) / 4;
+    long blocks = (count + ipw - 1) / ipw;                 // one warp (tile) per block
     if (blocks < l.blocks) l.blocks = (int)std::max(blocks, 1L);
   }
   hb::SqrArgs A;

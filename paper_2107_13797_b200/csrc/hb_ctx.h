@@ -134,24 +134,26 @@ inline Launch plan(const hb_ctx* ctx, int base, long count) {
   const int tpi = kCfgs[cfg].tpi, lpt = kCfgs[cfg].lpt;
   const int ipw = 32 / tpi;
   long ntiles = (count + ipw - 1) / ipw;
-  long blocks = (ntiles + 3) / 4;
-  long maxb = (long)ctx->sms * hb::blocks_per_sm(lpt);
-  if (blocks > maxb) blocks = maxb;
-  if (blocks < 1) blocks = 1;
+  long nwarps = ntiles;
+  const long maxw = (long)ctx->sms * hb::blocks_per_sm(lpt) * 4;
+  if (nwarps > maxw) nwarps = maxw;
+  if (nwarps < 1) nwarps = 1;
+  // One warp per block (4 * blocks_per_sm of them resident per SM): the grid-stride tile loop of every kernel then
+  // depends on blockIdx only, so the compiler knows the warp cannot diverge and emits bare SHFL instructions
+  // instead of a WARPSYNC.COLLECTIVE / ENDCOLLECTIVE bracket around each of the three shuffles per row.
   Launch l;
-  l.blocks = (int)blocks;
-  l.threads = 128;
+  l.blocks = (int)nwarps;
+  l.threads = 32;
   l.smem = 0;
-  (void)ipw;
-  l.nwarps = blocks * 4;
+  l.nwarps = nwarps;
   l.cfg = cfg;
   return l;
 }
 
 // Dynamic shared memory of the kernels that square through Mont::sqr (k_sqrmod; k_encrypt / k_decrypt under
-// -DHB_USE_SQR): 4 warps per block.
+// -DHB_USE_SQR): one warp per block.
 template <int LPT, int TPI>
-constexpr size_t sqr_smem_bytes() { return (size_t)hb::Mont<LPT, TPI>::SQ_WORDS * hb::Mont<LPT, TPI>::IPW * 4 * sizeof(uint32_t); }
+constexpr size_t sqr_smem_bytes() { return (size_t)hb::Mont<LPT, TPI>::SQ_WORDS * hb::Mont<LPT, TPI>::IPW * sizeof(uint32_t); }
 
 #define HB_SQR_CASE(KERNEL, LPT_, TPI_, launch, stream, args)                                                  \
   {                                                                                                          \

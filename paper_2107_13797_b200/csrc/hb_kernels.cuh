@@ -67,8 +67,7 @@ template <int LPT, int TPI>
 __device__ __forceinline__ uint32_t* sqr_scratch() {
   using M = Mont<LPT, TPI>;
   if constexpr (M::HAS_SQR) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    return hb_dyn_smem + warp * (M::SQ_WORDS * M::IPW) + lane / TPI;
+    return hb_dyn_smem + threadIdx.x / TPI;        // one warp per block
   } else {
     return nullptr;
   }
@@ -91,13 +90,15 @@ struct EncArgs {
 };
 
 template <int LPT, int TPI>
-__global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_encrypt(EncArgs A) {
+__global__ void __launch_bounds__(32, 4 * blocks_per_sm(LPT)) k_encrypt(EncArgs A) {
   using M = Mont<LPT, TPI>;
   constexpr int IPW = 32 / TPI;
   M mt;
   mt.init(A.mod.n, A.mod.np);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane / TPI;
-  const long wg = (long)blockIdx.x * (blockDim.x >> 5) + warp, nw = (long)gridDim.x * (blockDim.x >> 5);
+  // one warp per block: the tile loop then depends on blockIdx only, the compiler can see that the warp never
+  // diverges, and every __shfl_sync becomes a bare SHFL instead of a WARPSYNC.COLLECTIVE / ENDCOLLECTIVE bracket
+  const int lane = threadIdx.x, g = lane / TPI;
+  const long wg = blockIdx.x, nw = gridDim.x;
   uint32_t* tw = A.tbl + wg * A.tbl_stride;
   uint32_t* sw = sqr_scratch<LPT, TPI>();
   const long ntiles = (A.count + IPW - 1) / IPW;
@@ -138,13 +139,15 @@ struct MulArgs {
 };
 
 template <int LPT, int TPI>
-__global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_mulmod(MulArgs A) {
+__global__ void __launch_bounds__(32, 4 * blocks_per_sm(LPT)) k_mulmod(MulArgs A) {
   using M = Mont<LPT, TPI>;
   constexpr int IPW = 32 / TPI;
   M mt;
   mt.init(A.mod.n, A.mod.np);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane / TPI;
-  const long wg = (long)blockIdx.x * (blockDim.x >> 5) + warp, nw = (long)gridDim.x * (blockDim.x >> 5);
+  // one warp per block: the tile loop then depends on blockIdx only, the compiler can see that the warp never
+  // diverges, and every __shfl_sync becomes a bare SHFL instead of a WARPSYNC.COLLECTIVE / ENDCOLLECTIVE bracket
+  const int lane = threadIdx.x, g = lane / TPI;
+  const long wg = blockIdx.x, nw = gridDim.x;
   const long ntiles = (A.count + IPW - 1) / IPW;
   for (long tile = wg; tile < ntiles; tile += nw) {
     long inst = tile * IPW + g;
@@ -182,13 +185,15 @@ struct PlainArgs {
 
 // Plaintext-side residue arithmetic mod n (batches.py:173-205 of the reference: plain_mul, plain_add).
 template <int LPT, int TPI>
-__global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_plainop(PlainArgs A) {
+__global__ void __launch_bounds__(32, 4 * blocks_per_sm(LPT)) k_plainop(PlainArgs A) {
   using M = Mont<LPT, TPI>;
   constexpr int IPW = 32 / TPI;
   M mt;
   mt.init(A.mod.n, A.mod.np);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane / TPI;
-  const long wg = (long)blockIdx.x * (blockDim.x >> 5) + warp, nw = (long)gridDim.x * (blockDim.x >> 5);
+  // one warp per block: the tile loop then depends on blockIdx only, the compiler can see that the warp never
+  // diverges, and every __shfl_sync becomes a bare SHFL instead of a WARPSYNC.COLLECTIVE / ENDCOLLECTIVE bracket
+  const int lane = threadIdx.x, g = lane / TPI;
+  const long wg = blockIdx.x, nw = gridDim.x;
   const long ntiles = (A.count + IPW - 1) / IPW;
   for (long tile = wg; tile < ntiles; tile += nw) {
     long inst = tile * IPW + g;
@@ -221,13 +226,15 @@ struct SqrArgs {
 
 // out[i] = a[i]^(2^reps) mod n^2 through the squaring path of the shape (Mont::sqr where there is one).
 template <int LPT, int TPI>
-__global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_sqrmod(SqrArgs A) {
+__global__ void __launch_bounds__(32, 4 * blocks_per_sm(LPT)) k_sqrmod(SqrArgs A) {
   using M = Mont<LPT, TPI>;
   constexpr int IPW = 32 / TPI;
   M mt;
   mt.init(A.mod.n, A.mod.np);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane / TPI;
-  const long wg = (long)blockIdx.x * (blockDim.x >> 5) + warp, nw = (long)gridDim.x * (blockDim.x >> 5);
+  // one warp per block: the tile loop then depends on blockIdx only, the compiler can see that the warp never
+  // diverges, and every __shfl_sync becomes a bare SHFL instead of a WARPSYNC.COLLECTIVE / ENDCOLLECTIVE bracket
+  const int lane = threadIdx.x, g = lane / TPI;
+  const long wg = blockIdx.x, nw = gridDim.x;
   uint32_t* sw = sqr_scratch<LPT, TPI>();
   const long ntiles = (A.count + IPW - 1) / IPW;
   for (long tile = wg; tile < ntiles; tile += nw) {
@@ -278,12 +285,14 @@ struct DecArgs {
 };
 
 template <int LPT, int TPI>
-__global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_decrypt(DecArgs A) {
+__global__ void __launch_bounds__(32, 4 * blocks_per_sm(LPT)) k_decrypt(DecArgs A) {
   using M = Mont<LPT, TPI>;
   constexpr int IPW = 32 / TPI;
   M mt;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane / TPI;
-  const long wg = (long)blockIdx.x * (blockDim.x >> 5) + warp, nw = (long)gridDim.x * (blockDim.x >> 5);
+  // one warp per block: the tile loop then depends on blockIdx only, the compiler can see that the warp never
+  // diverges, and every __shfl_sync becomes a bare SHFL instead of a WARPSYNC.COLLECTIVE / ENDCOLLECTIVE bracket
+  const int lane = threadIdx.x, g = lane / TPI;
+  const long wg = blockIdx.x, nw = gridDim.x;
   uint32_t* tw = A.tbl + wg * A.tbl_stride;
   uint32_t* sw = sqr_scratch<LPT, TPI>();
   const long ntiles = (A.count + IPW - 1) / IPW;

@@ -17,16 +17,16 @@ namespace hb {
   using M = Mont<LPT, TPI>;                                                                      \
   constexpr int IPW = 32 / TPI;                                                                  \
   constexpr int L = LPT * TPI;                                                                   \
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane / TPI;                    \
-  const long wg = (long)blockIdx.x * (blockDim.x >> 5) + warp, nw = (long)gridDim.x * (blockDim.x >> 5); \
-  (void)L; (void)g; (void)wg; (void)nw;
+  const int lane = threadIdx.x, g = lane / TPI;            /* one warp per block, see hb_ctx.h plan() */ \
+  const long wg = blockIdx.x, nw = gridDim.x;                                                    \
+  (void)L; (void)g; (void)wg; (void)nw; (void)lane;
 
 // ------------------------------------------------------------------------------------------------
 // words -> Montgomery digit form
 struct ToMontArgs { ModDev mod; const uint32_t* words; int w; uint32_t* dig; long count; };
 
 template <int LPT, int TPI>
-__global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_to_mont(ToMontArgs A) {
+__global__ void __launch_bounds__(32, 4 * blocks_per_sm(LPT)) k_to_mont(ToMontArgs A) {
   HB_GROUP_PROLOGUE(LPT, TPI)
   M mt;
   mt.init(A.mod.n, A.mod.np);
@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_to_mont(ToMontArgs 
 struct FromMontArgs { ModDev mod; const uint32_t* dig; long count; uint32_t* words; int w; };
 
 template <int LPT, int TPI>
-__global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_from_mont(FromMontArgs A) {
+__global__ void __launch_bounds__(32, 4 * blocks_per_sm(LPT)) k_from_mont(FromMontArgs A) {
   HB_GROUP_PROLOGUE(LPT, TPI)
   M mt;
   mt.init(A.mod.n, A.mod.np);
@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_from_mont(FromMontA
 struct PairUpArgs { ModDev mod; const uint32_t* src; long nsrc; uint32_t* dst; };
 
 template <int LPT, int TPI>
-__global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_pair_up(PairUpArgs A) {
+__global__ void __launch_bounds__(32, 4 * blocks_per_sm(LPT)) k_pair_up(PairUpArgs A) {
   HB_GROUP_PROLOGUE(LPT, TPI)
   M mt;
   mt.init(A.mod.n, A.mod.np);
@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_pair_up(PairUpArgs 
 struct PairDownArgs { ModDev mod; const uint32_t* inv_parent; const uint32_t* val_child; long nchild; uint32_t* inv_child; };
 
 template <int LPT, int TPI>
-__global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_pair_down(PairDownArgs A) {
+__global__ void __launch_bounds__(32, 4 * blocks_per_sm(LPT)) k_pair_down(PairDownArgs A) {
   HB_GROUP_PROLOGUE(LPT, TPI)
   M mt;
   mt.init(A.mod.n, A.mod.np);
@@ -340,7 +340,7 @@ struct PowVarArgs {
 };
 
 template <int LPT, int TPI>
-__global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_powvar(PowVarArgs A) {
+__global__ void __launch_bounds__(32, 4 * blocks_per_sm(LPT)) k_powvar(PowVarArgs A) {
   HB_GROUP_PROLOGUE(LPT, TPI)
   M mt;
   mt.init(A.mod.n, A.mod.np);
@@ -431,7 +431,7 @@ struct ProductArgs {
 };
 
 template <int LPT, int TPI>
-__global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_product_pass(ProductArgs A) {
+__global__ void __launch_bounds__(32, 4 * blocks_per_sm(LPT)) k_product_pass(ProductArgs A) {
   HB_GROUP_PROLOGUE(LPT, TPI)
   M mt;
   mt.init(A.mod.n, A.mod.np);
@@ -534,7 +534,7 @@ struct SegArgs {
 };
 
 template <int LPT, int TPI>
-__global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_bucket_segments(SegArgs A) {
+__global__ void __launch_bounds__(32, 4 * blocks_per_sm(LPT)) k_bucket_segments(SegArgs A) {
   HB_GROUP_PROLOGUE(LPT, TPI)
   M mt;
   mt.init(A.mod.n, A.mod.np);
@@ -590,7 +590,7 @@ struct CombineArgs {
 };
 
 template <int LPT, int TPI>
-__global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_bucket_combine(CombineArgs A) {
+__global__ void __launch_bounds__(32, 4 * blocks_per_sm(LPT)) k_bucket_combine(CombineArgs A) {
   HB_GROUP_PROLOGUE(LPT, TPI)
   M mt;
   mt.init(A.mod.n, A.mod.np);
@@ -644,7 +644,7 @@ struct RunningArgs {
 };
 
 template <int LPT, int TPI>
-__global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_bucket_running(RunningArgs A) {
+__global__ void __launch_bounds__(32, 4 * blocks_per_sm(LPT)) k_bucket_running(RunningArgs A) {
   HB_GROUP_PROLOGUE(LPT, TPI)
   M mt;
   mt.init(A.mod.n, A.mod.np);
@@ -679,7 +679,7 @@ struct HornerArgs {
 };
 
 template <int LPT, int TPI>
-__global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_window_horner(HornerArgs A) {
+__global__ void __launch_bounds__(32, 4 * blocks_per_sm(LPT)) k_window_horner(HornerArgs A) {
   HB_GROUP_PROLOGUE(LPT, TPI)
   M mt;
   mt.init(A.mod.n, A.mod.np);
@@ -707,7 +707,7 @@ __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_window_horner(Horne
 struct FoldArgs { ModDev mod; const uint32_t* src; long rstride; int nr; long count; uint32_t* dst; };
 
 template <int LPT, int TPI>
-__global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_fold(FoldArgs A) {
+__global__ void __launch_bounds__(32, 4 * blocks_per_sm(LPT)) k_fold(FoldArgs A) {
   HB_GROUP_PROLOGUE(LPT, TPI)
   M mt;
   mt.init(A.mod.n, A.mod.np);
@@ -731,7 +731,7 @@ __global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_fold(FoldArgs A) {
 struct FinishArgs { ModDev mod; const uint32_t* ab; const uint32_t* binv; int d; uint32_t* out; int wc; };
 
 template <int LPT, int TPI>
-__global__ void __launch_bounds__(128, blocks_per_sm(LPT)) k_matvec_finish(FinishArgs A) {
+__global__ void __launch_bounds__(32, 4 * blocks_per_sm(LPT)) k_matvec_finish(FinishArgs A) {
   HB_GROUP_PROLOGUE(LPT, TPI)
   M mt;
   mt.init(A.mod.n, A.mod.np);
