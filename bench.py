@@ -48,6 +48,7 @@ def parse_args():
     ap.add_argument("--no-matvec", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-flr", action="store_true")
+    ap.add_argument("--no-ops", action="store_true", help="skip the per-operator rates in extras")
     ap.add_argument("--flr-rows", type=int, default=50_000,
                     help="rows of the heterogeneous-FLR extra (BASELINE configs[3] shape, 200 features)")
     return ap.parse_args()
@@ -332,6 +333,48 @@ def run_b200(args):
         extras["matvec_terms_per_s"] = terms / (mv_ms * 1e-3)
         # canonical work: (1.25 * 52 + 1) modmuls per term (SURVEY.md 8d, 52-bit scalars)
         extras["matvec_canonical_lp_per_s"] = terms * (1.25 * 52 + 1) * LP_MODMUL / (mv_ms * 1e-3)
+
+    # ---- extra: the other six operators of the reference's own harness (bench.py:65-101 of the reference:
+    # encode, decode, hmul, hadd, hsum next to henc / hdec / hmatmul), each on this rank's `count` elements
+    if not args.no_ops:
+        def timed(fn, reps=2):
+            fn()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            a.record()
+            for _ in range(reps):
+                fn()
+            b.record()
+            b.synchronize()
+            return a.elapsed_time(b) * 1e-3 / reps
+
+        tmp_c = torch.empty((count, wc), dtype=torch.int32, device="cuda")
+        tmp_m = torch.empty((count, wn), dtype=torch.int32, device="cuda")
+        tmp_f = torch.empty(count, dtype=torch.float64, device="cuda")
+        one_c = torch.empty((1, wc), dtype=torch.int32, device="cuda")
+        t_enc = timed(lambda: _native.check(lib.hb_encode_f64(ctx.handle, vals.data_ptr(), -8, tmp_m.data_ptr(), count,
+                                                              bad.data_ptr(), stream)), reps=20)
+        t_dec = timed(lambda: _native.check(lib.hb_decode_f64(ctx.handle, m.data_ptr(), -8, tmp_f.data_ptr(), count,
+                                                              bad.data_ptr(), stream)), reps=20)
+        if not torch.equal(tmp_m, m):
+            raise SystemExit("codec is not deterministic")
+        grid = torch.round(vals * 4294967296.0) / 4294967296.0          # exponent -8: the 16^-8 = 2^-32 grid
+        if not torch.equal(tmp_f, grid):
+            raise SystemExit("decode(encode(v)) is not v rounded to the 16^-8 grid")
+        t_add = timed(lambda: _native.check(lib.hb_mulmod(ctx.handle, c.data_ptr(), c.data_ptr(), tmp_c.data_ptr(),
+                                                          count, 0, stream)))
+        # scalars = the encoded values themselves: 39-bit magnitudes, half of them negative residues (inverse base)
+        t_mul = timed(lambda: _native.check(lib.hb_powscalar(ctx.handle, c.data_ptr(), m.data_ptr(), tmp_c.data_ptr(),
+                                                             count, count, 0, stream)), reps=1)
+        t_sum = timed(lambda: _native.check(lib.hb_product(ctx.handle, c.data_ptr(), one_c.data_ptr(), 1, count, 0, 1,
+                                                           stream)))
+        codec_bytes = count * (8 + 4 * wn)
+        extras["operators_per_s_per_gpu"] = {
+            "encode": count / t_enc, "decode": count / t_dec, "hadd": count / t_add, "hmul_39bit_signed": count / t_mul,
+            "hsum_elements": count / t_sum}
+        extras["codec_hbm_frac"] = {"encode": codec_bytes / t_enc / 1e9 / _hbm_peak(),
+                                    "decode": codec_bytes / t_dec / 1e9 / _hbm_peak()}
+        del tmp_c, tmp_m, tmp_f
 
     # ---- extra: one full-batch iteration of heterogeneous FLR (BASELINE configs[3] shape at reduced rows)
     if not args.no_flr and world == 1 and count >= 100_000:

@@ -113,6 +113,8 @@ int hb_ctx_create(hb_ctx** out, const uint32_t* n_words, int n_nwords, int devic
       Big mi = third;
       mi.resize(ctx->wn, 0);
       ctx->off_maxint = cb.add(mi);
+      ctx->maxint_top = 0;
+      for (int i = 0; i < ctx->wn; i++) if (mi[i]) ctx->maxint_top = i;
     }
     Big nb = n;
     hbh::sub_in(nb, third);
@@ -180,6 +182,7 @@ void hb_ctx_destroy(hb_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->d_pub) cudaFree(ctx->d_pub);
   if (ctx->d_priv) cudaFree(ctx->d_priv);
+  if (ctx->codec_scratch) cudaFree(ctx->codec_scratch);
   delete ctx;
 }
 

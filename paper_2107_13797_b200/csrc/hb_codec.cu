@@ -17,7 +17,13 @@ struct CodecArgs {
   const double* fin; double* fout;
   const uint32_t* min; uint32_t* mout;
   unsigned long long* first_bad;
+  int maxint_top;            // index of the highest non-zero word of max_int
+  uint8_t* slow;             // decode: fast kernel marks the elements it leaves to the generic kernel
+  const uint8_t* only;       // decode: generic kernel handles marked elements only (nullptr = all)
+  unsigned long long* nslow; // decode: how many elements were marked
 };
+
+__device__ __forceinline__ uint4 ld4(const uint32_t* p) { return *reinterpret_cast<const uint4*>(p); }
 
 // round(v * 16^-exponent) half-to-even, |.| < max_int, stored as a residue mod n (encoding.py:72-78)
 __global__ void __launch_bounds__(64) k_encode_f64(CodecArgs A) {
@@ -94,13 +100,19 @@ __global__ void __launch_bounds__(64) k_decode_f64(CodecArgs A) {
   const int wn = A.wn, pitch = wn + 1;
   const long base = (long)blockIdx.x * blockDim.x;
   const long nhere = min((long)blockDim.x, A.count - base);
+  bool mine = true;
+  if (A.only) {
+    if (*A.nslow == 0ull) return;               // the usual case: the wide kernel handled everything
+    mine = base + threadIdx.x < A.count && A.only[base + threadIdx.x] != 0;
+    if (!__syncthreads_or(mine)) return;        // nothing in this block was left to the generic path
+  }
   for (long idx = threadIdx.x; idx < nhere * wn; idx += blockDim.x) {
     long el = idx / wn; int w = (int)(idx - el * wn);
     stage[el * pitch + w] = A.min[(base + el) * wn + w];
   }
   __syncthreads();
   const long e = base + threadIdx.x;
-  if (e >= A.count) return;
+  if (e >= A.count || !mine) return;
   uint32_t* my = stage + threadIdx.x * pitch;
   int c_max = 0, c_neg = 0;     // compare with max_int and with n - max_int
   for (int i = wn - 1; i >= 0; i--) {
@@ -150,6 +162,212 @@ __global__ void __launch_bounds__(64) k_decode_f64(CodecArgs A) {
     val = ldexp((double)m53, ex2 + 4 * A.exponent);
   }
   A.fout[e] = neg ? -val : val;
+}
+
+
+// ---- HBM-bound forms of the two codec kernels ----------------------------------------------------------------
+//
+// A residue is 4 * wn bytes of which, for every value a protocol ever encodes, all but three words are either zero
+// (positive) or the words of n (negative, n - |x|).  The thread-per-element kernels above spend hundreds of
+// instructions per element walking those words; the kernels below move the background with 16-byte accesses, 16
+// lanes per element, and leave only the three interesting words to one thread per element.  Requires wn % 4 == 0
+// and wn >= 8 (the host falls back to the kernels above otherwise).
+
+// encode: pass 1 stores the background (0 or n), pass 2 patches the up-to-three magnitude words and the borrow run
+__global__ void __launch_bounds__(256) k_encode_f64_wide(CodecArgs A) {
+  const int lane = threadIdx.x & 31;
+  const long warp = (long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const long nwarps = (long)gridDim.x * (blockDim.x >> 5);
+  const int wn = A.wn, T = A.maxint_top;
+  for (long eb = warp * 32; eb < A.count; eb += nwarps * 32) {
+    const long e = eb + lane;
+    const bool have = e < A.count;
+    const unsigned long long bits = have ? (unsigned long long)__double_as_longlong(A.fin[e]) : 0ull;
+    const bool negv = (bits >> 63) != 0;
+    const int e11 = (int)((bits >> 52) & 0x7ff);
+    unsigned long long mant = bits & 0xfffffffffffffull;
+    int e2;
+    if (e11 == 0) e2 = -1074; else { mant |= 1ull << 52; e2 = e11 - 1075; }
+    long shift = (long)e2 - 4L * A.exponent;      // scaled = mant * 2^shift
+    if (shift < 0) {
+      long s = -shift;
+      if (s >= 64) mant = 0;
+      else {
+        unsigned long long q = mant >> s, rem = mant & ((1ull << s) - 1ull), half = 1ull << (s - 1);
+        if (rem > half || (rem == half && (q & 1ull))) q++;
+        mant = q;
+      }
+      shift = 0;
+    }
+    if (mant == 0) shift = 0;
+    const long ws = shift >> 5; const int bs = (int)(shift & 31);
+    const unsigned long long lo = mant << bs;
+    uint32_t v0 = (uint32_t)lo, v1 = (uint32_t)(lo >> 32), v2 = bs ? (uint32_t)(mant >> (64 - bs)) : 0u;
+    // |scaled| >= max_int ?  Decided by the position of the top word except when both top words coincide.
+    const long tw = mant ? ws + (v2 ? 2 : v1 ? 1 : 0) : -1;
+    bool over = tw > T;
+    if (tw == T) {
+      int cmp = 0;
+      for (long i = T; i >= 0 && cmp == 0; i--) {
+        const long r = i - ws;
+        const uint32_t a = r == 0 ? v0 : r == 1 ? v1 : r == 2 ? v2 : 0u, b = A.maxint[i];
+        cmp = a > b ? 1 : (a < b ? -1 : 0);
+      }
+      over = cmp >= 0;
+    }
+    if (have && over) atomicMin(A.first_bad, (unsigned long long)e);
+    const bool neg = have && negv && mant != 0 && !over;
+    long bend = 0;
+    bool brun = false;
+    if (neg) {                                     // n - |scaled| on the three words, borrow runs on through zero words of n
+      uint32_t borrow = 0;
+      uint32_t* vs[3] = {&v0, &v1, &v2};
+#pragma unroll
+      for (int k = 0; k < 3; k++) {
+        const uint32_t nk = ws + k < wn ? A.nwords[ws + k] : 0u;
+        const unsigned long long d = (unsigned long long)nk - *vs[k] - borrow;
+        borrow = (uint32_t)(d >> 63);
+        *vs[k] = (uint32_t)d;
+      }
+      if (borrow) {
+        brun = true;
+        bend = ws + 3;
+        while (bend < wn && A.nwords[bend] == 0u) bend++;
+      }
+    }
+    // pass 1: background, two elements per step, 16 lanes x 16 bytes each
+    const uint32_t negmask = __ballot_sync(0xffffffffu, neg);
+    const int half = lane >> 4, l16 = lane & 15;
+    for (int s = 0; s < 32; s += 2) {
+      const int src = s + half;
+      const long ee = eb + src;
+      if (ee < A.count) {
+        const bool isneg = (negmask >> src) & 1u;
+        uint32_t* dst = A.mout + ee * wn;
+        for (int i0 = 4 * l16; i0 < wn; i0 += 64) {
+          uint4 val = make_uint4(0u, 0u, 0u, 0u);
+          if (isneg) val = ld4(A.nwords + i0);
+          *reinterpret_cast<uint4*>(dst + i0) = val;
+        }
+      }
+    }
+    __syncwarp();
+    // pass 2: the words that differ from the background
+    if (have && !over) {
+      uint32_t* dst = A.mout + e * wn;
+      if (ws < wn) dst[ws] = v0;
+      if (ws + 1 < wn) dst[ws + 1] = v1;
+      if (ws + 2 < wn) dst[ws + 2] = v2;
+      if (brun) {
+        for (long i = ws + 3; i < bend; i++) dst[i] = 0xffffffffu;
+        if (bend < wn) dst[bend] = A.nwords[bend] - 1u;
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// decode: pass 1 checks that every word from the fourth up is background (all zero, or all equal to n); pass 2
+// turns the low 96 bits into the correctly rounded double.  Anything else -- wide magnitudes, the overflow band --
+// is marked in A.slow for the generic kernel.  Needs max_int >= 2^96 (maxint_top >= 3).
+__global__ void __launch_bounds__(256, 4) k_decode_f64_wide(CodecArgs A) {
+  const int lane = threadIdx.x & 31;
+  const long warp = (long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const long nwarps = (long)gridDim.x * (blockDim.x >> 5);
+  const int wn = A.wn;
+  const int half = lane >> 4, l16 = lane & 15;
+  const int i0 = 4 * l16;
+  uint4 nv0 = make_uint4(0u, 0u, 0u, 0u), nv1 = nv0;             // this lane's words of n (chunks 0 and 1)
+  if (i0 < wn) nv0 = ld4(A.nwords + i0);
+  if (i0 + 64 < wn) nv1 = ld4(A.nwords + i0 + 64);
+  for (long eb = warp * 32; eb < A.count; eb += nwarps * 32) {
+    // own element's low words first: their latency hides behind pass 1
+    const long e = eb + lane;
+    uint32_t m0 = 0, m1 = 0, m2 = 0;
+    if (e < A.count) {
+      const uint32_t* x = A.min + e * wn;
+      m0 = x[0]; m1 = x[1]; m2 = x[2];
+    }
+    bool my_zero = false, my_n = false;
+    for (int s = 0; s < 32; s += 8) {                             // four steps of two elements, loads issued together
+      uint4 xa[4], xb[4];
+      bool in[4];
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        const long ee = eb + s + 2 * j + half;
+        in[j] = ee < A.count;
+        xa[j] = nv0;
+        xb[j] = nv1;
+        if (in[j] && i0 < wn) xa[j] = ld4(A.min + ee * wn + i0);
+        if (in[j] && i0 + 64 < wn) xb[j] = ld4(A.min + ee * wn + i0 + 64);
+      }
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        bool zero_ok = true, n_ok = true;
+        if (in[j] && i0 < wn) {
+          if (i0 == 0) {
+            zero_ok = xa[j].w == 0u;
+            n_ok = xa[j].w == nv0.w;
+          } else {
+            zero_ok = (xa[j].x | xa[j].y | xa[j].z | xa[j].w) == 0u;
+            n_ok = xa[j].x == nv0.x && xa[j].y == nv0.y && xa[j].z == nv0.z && xa[j].w == nv0.w;
+          }
+        }
+        if (in[j] && i0 + 64 < wn) {
+          zero_ok &= (xb[j].x | xb[j].y | xb[j].z | xb[j].w) == 0u;
+          n_ok &= xb[j].x == nv1.x && xb[j].y == nv1.y && xb[j].z == nv1.z && xb[j].w == nv1.w;
+        }
+        const uint32_t bz = __ballot_sync(0xffffffffu, zero_ok), bn = __ballot_sync(0xffffffffu, n_ok);
+        const int first = s + 2 * j;
+        if (lane == first) { my_zero = (bz & 0xffffu) == 0xffffu; my_n = (bn & 0xffffu) == 0xffffu; }
+        if (lane == first + 1) { my_zero = (bz >> 16) == 0xffffu; my_n = (bn >> 16) == 0xffffu; }
+      }
+    }
+    if (e >= A.count) continue;
+    bool neg = false, slow = false;
+    if (my_zero) {
+      // positive, below 2^96 <= max_int
+    } else if (my_n) {
+      unsigned long long d = (unsigned long long)A.nwords[0] - m0;
+      m0 = (uint32_t)d;
+      d = (unsigned long long)A.nwords[1] - m1 - (d >> 63);
+      m1 = (uint32_t)d;
+      d = (unsigned long long)A.nwords[2] - m2 - (d >> 63);
+      m2 = (uint32_t)d;
+      neg = true;
+      slow = (d >> 63) != 0 || (m0 | m1 | m2) == 0u;     // x >= n: not a residue; let the generic path judge it
+    } else {
+      slow = true;
+    }
+    A.slow[e] = slow ? 1 : 0;
+    if (slow) { atomicAdd(A.nslow, 1ull); continue; }
+    double val = 0.0;
+    if (m0 | m1 | m2) {
+      const int tb = m2 ? 95 - __clz(m2) : m1 ? 63 - __clz(m1) : 31 - __clz(m0);
+      const unsigned long long low = (unsigned long long)m0 | ((unsigned long long)m1 << 32);
+      unsigned long long m53;
+      int ex2 = 0;
+      if (tb <= 52) {
+        m53 = low;
+      } else {
+        unsigned long long win;
+        bool sticky = false;
+        if (tb <= 63) {
+          win = low << (63 - tb);
+        } else {
+          const int sh = tb - 63;                        // 1..32
+          win = (low >> sh) | ((unsigned long long)m2 << (64 - sh));
+          sticky = (low & ((1ull << sh) - 1ull)) != 0ull;
+        }
+        m53 = win >> 11;
+        const unsigned long long rem = win & 0x7ffull, halfway = 0x400ull;
+        if (rem > halfway || (rem == halfway && (sticky || (m53 & 1ull)))) m53++;
+        ex2 = tb - 52;
+      }
+      val = ldexp((double)m53, ex2 + 4 * A.exponent);
+    }
+    A.fout[e] = neg ? -val : val;
+  }
 }
 
 // Exact re-grid onto a finer exponent (encoding.py:104-113): signed mantissa times 16^digits, range-checked
@@ -257,9 +475,16 @@ int hb_encode_f64(hb_ctx* ctx, const double* values, int exponent, uint32_t* m_o
   A.nwords = ctx->d_pub + ctx->off_nwords; A.maxint = ctx->d_pub + ctx->off_maxint;
   A.negband = ctx->d_pub + ctx->off_negband; A.wn = ctx->wn; A.exponent = exponent; A.count = count;
   A.fin = values; A.mout = m_out; A.first_bad = (unsigned long long*)first_bad;
-  const int threads = 64;
-  const size_t smem = (size_t)threads * (ctx->wn + 1) * sizeof(uint32_t);
-  hb::k_encode_f64<<<(unsigned)((count + threads - 1) / threads), threads, smem, (cudaStream_t)stream_>>>(A);
+  A.maxint_top = ctx->maxint_top;
+  if (ctx->wn % 4 == 0 && ctx->wn >= 8) {
+    const long warps = (count + 31) / 32;
+    const long blocks = std::min<long>((warps + 7) / 8, (long)ctx->sms * 8);
+    hb::k_encode_f64_wide<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream_>>>(A);
+  } else {
+    const int threads = 64;
+    const size_t smem = (size_t)threads * (ctx->wn + 1) * sizeof(uint32_t);
+    hb::k_encode_f64<<<(unsigned)((count + threads - 1) / threads), threads, smem, (cudaStream_t)stream_>>>(A);
+  }
   g_launches++;
   CU(cudaGetLastError());
   return HB_OK;
@@ -275,9 +500,31 @@ int hb_decode_f64(hb_ctx* ctx, const uint32_t* m, int exponent, double* values_o
   A.nwords = ctx->d_pub + ctx->off_nwords; A.maxint = ctx->d_pub + ctx->off_maxint;
   A.negband = ctx->d_pub + ctx->off_negband; A.wn = ctx->wn; A.exponent = exponent; A.count = count;
   A.min = m; A.fout = values_out; A.first_bad = (unsigned long long*)first_bad;
+  A.maxint_top = ctx->maxint_top;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  if (ctx->wn % 4 == 0 && ctx->wn >= 8 && ctx->wn <= 128 && ctx->maxint_top >= 3) {
+    if (ctx->codec_cap < (size_t)count + 16) {          // grows rarely; calls on one context use one stream at a time
+      CU(cudaStreamSynchronize(stream));
+      if (ctx->codec_scratch) CU(cudaFree(ctx->codec_scratch));
+      ctx->codec_scratch = nullptr;
+      ctx->codec_cap = 0;
+      const size_t cap = ((size_t)count + 16) * 5 / 4;
+      CU(cudaMalloc(&ctx->codec_scratch, cap));
+      ctx->codec_cap = cap;
+    }
+    uint8_t* slow = ctx->codec_scratch + 16;
+    A.slow = slow;
+    A.nslow = (unsigned long long*)ctx->codec_scratch;
+    CU(cudaMemsetAsync(ctx->codec_scratch, 0, 8, stream));
+    const long warps = (count + 31) / 32;
+    const long blocks = std::min<long>((warps + 7) / 8, (long)ctx->sms * 4);
+    hb::k_decode_f64_wide<<<(unsigned)blocks, 256, 0, stream>>>(A);
+    g_launches++;
+    A.only = slow;
+  }
   const int threads = 64;
   const size_t smem = (size_t)threads * (ctx->wn + 1) * sizeof(uint32_t);
-  hb::k_decode_f64<<<(unsigned)((count + threads - 1) / threads), threads, smem, (cudaStream_t)stream_>>>(A);
+  hb::k_decode_f64<<<(unsigned)((count + threads - 1) / threads), threads, smem, stream>>>(A);
   g_launches++;
   CU(cudaGetLastError());
   return HB_OK;

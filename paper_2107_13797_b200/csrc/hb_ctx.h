@@ -107,6 +107,9 @@ struct hb_ctx {
   size_t off_nR = 0, off_prog_n = 0;
   size_t off_nwords = 0, off_negband = 0, off_maxint = 0, off_n2words = 0;   // n, n - n/3 (wn words); n^2 padded for k_root_inverse
   int nprog_n = 0, slots_n = 0;
+  int maxint_top = 0;          // index of the highest non-zero word of max_int = n / 3
+  uint8_t* codec_scratch = nullptr;   // decode: [0, 8) count of elements left to the generic kernel, [16, ..) marks
+  size_t codec_cap = 0;
   int cfg_n = -1;              // limb shape for arithmetic mod n (plaintext side)
   hbi::ModOff mod_n_pub;
   // private part

@@ -166,14 +166,17 @@ int product_impl(hb_ctx* ctx, const uint32_t* c, int win, uint32_t* out, long ng
   const int cfg = ctx->cfg_pub;
   Scratch sc(stream);
   const uint32_t* src = c;
-  const long target = (long)ctx->sms * 64;      // work items that fill the machine
   while (true) {
+    // One chunk per resident instance slot where the data allows it: a single full wave per pass, and chunks long
+    // enough (>= 8) that the R^clen repair -- log2(clen) + 2 multiplications per work item -- stays small.
+    const int shape = kernel_cfg(cfg, ngroups * ((glen + 7) / 8));
+    const long slots = (long)ctx->sms * hb::blocks_per_sm(kCfgs[shape].lpt) * 4 * (32 / kCfgs[shape].tpi);
     long clen;
     if (glen <= 8) {
       clen = glen;
     } else {
-      clen = 8;
-      while (clen < 64 && ngroups * ((glen + clen - 1) / clen) > 4 * target) clen *= 2;
+      const long parts_wanted = std::max<long>(1, slots / std::max<long>(1, ngroups));
+      clen = std::max<long>(8, (glen + parts_wanted - 1) / parts_wanted);
     }
     long parts = (glen + clen - 1) / clen;
     uint32_t* dst = out;

@@ -473,3 +473,50 @@ def test_plain_rescale_overflow(okeys):
         if fit:
             ok_batch = PlaintextBatch(pk, (2,), (0,), (fit, n - fit), True)
             assert plain_rescale(ok_batch, -1).mantissas == (fit * 16, n - fit * 16)
+
+
+@pytest.mark.parametrize("bits", [256, 512, 1024, 2048, 3072])
+def test_codec_wide_kernels_edges(bits):
+    """The 16-byte-access codec kernels (hb_codec.cu, k_*_wide) on their edges: magnitudes around 2^96 (where decode
+    hands over to the generic kernel), sparse moduli whose zero words make the n - |x| borrow run long, values next
+    to max_int, both signs, mixed with ordinary values in one batch."""
+    from paper_2107_13797_b200.encoding import FixedPointOverflow
+    rng = random.Random(bits)
+    moduli = [rng.getrandbits(bits) | (1 << (bits - 1)) | 1,
+              (1 << (bits - 1)) + 12345,                               # words 1 .. wn-2 are zero
+              (1 << (bits - 1)) + (1 << 160) + 1,                      # zero words between 0 and 5, and above 5
+              (1 << bits) - 1 - (1 << 40)]
+    for n in moduli:
+        ok = ho.Key(n)
+        pk = paillier.PublicKey(n)
+        # encode: ordinary doubles, tiny and huge ones, exact ties; every exponent moves the three words elsewhere
+        vals = [rng.uniform(-100.0, 100.0) for _ in range(70)] + [0.0, -0.0, 1.0, -1.0, 2.0 ** -40, -2.0 ** -40,
+                                                                  2.0 ** 52 + 1, -(2.0 ** 53 - 1), 1.5, -2.5, 3e15, -7e15]
+        for exponent in (-8, 0, 5, -13, -24):
+            want = [ho.encode(ok, v, exponent)[0] for v in vals]
+            got = ops.batch_encode(pk, vals, exponent)
+            assert list(got.mantissas) == want, (bits, hex(n)[:12], exponent)
+            assert ops.batch_decode(pk, got) == [ho.decode(ok, m, exponent) for m in want]
+        # decode: magnitudes around the 96-bit hand-over and up to max_int, both signs
+        mags = [0, 1, 2 ** 53 - 1, 2 ** 53, 2 ** 53 + 1, 2 ** 64 - 1, 2 ** 64, 2 ** 95, 2 ** 96 - 1, 2 ** 96, 2 ** 96 + 1,
+                2 ** 97 - 1, 3 * 2 ** 94 + 2 ** 41, 2 ** 96 - 2 ** 42 - 1, ok.max_int - 1, ok.max_int // 2 + 1]
+        mags += [rng.getrandbits(rng.randrange(1, 130)) for _ in range(60)]
+        mags = [m for m in mags if m < ok.max_int and m < 2 ** 900]      # beyond that the double overflows
+        res = mags + [(n - m) % n for m in mags if m]
+        rng.shuffle(res)
+        for exponent in (-8, -30, 0):
+            pb = PlaintextBatch(pk, (len(res),), (exponent,), tuple(res), True)
+            assert ops.batch_decode(pk, pb) == [ho.decode(ok, m, exponent) for m in res], (bits, hex(n)[:12], exponent)
+        # overflow band in the middle of a batch of fast-path elements
+        band = res[:40] + [ok.max_int] + res[40:80]
+        with pytest.raises(FixedPointOverflow):
+            ops.batch_decode(pk, PlaintextBatch(pk, (len(band),), (0,), tuple(band), True))
+        band[40] = n - ok.max_int
+        with pytest.raises(FixedPointOverflow):
+            ops.batch_decode(pk, PlaintextBatch(pk, (len(band),), (0,), tuple(band), True))
+        # encode overflow exactly at max_int when it is representable as a double
+        if bits == 256:
+            edge = float(ok.max_int)
+            if int(edge) >= ok.max_int:
+                with pytest.raises(FixedPointOverflow):
+                    ops.batch_encode(pk, [1.0, edge], 0)
