@@ -94,26 +94,10 @@ __global__ void __launch_bounds__(64) k_encode_f64(CodecArgs A) {
   }
 }
 
-// residue -> signed mantissa -> correctly rounded double (encoding.py:81-101)
-__global__ void __launch_bounds__(64) k_decode_f64(CodecArgs A) {
-  extern __shared__ uint32_t stage[];
-  const int wn = A.wn, pitch = wn + 1;
-  const long base = (long)blockIdx.x * blockDim.x;
-  const long nhere = min((long)blockDim.x, A.count - base);
-  bool mine = true;
-  if (A.only) {
-    if (*A.nslow == 0ull) return;               // the usual case: the wide kernel handled everything
-    mine = base + threadIdx.x < A.count && A.only[base + threadIdx.x] != 0;
-    if (!__syncthreads_or(mine)) return;        // nothing in this block was left to the generic path
-  }
-  for (long idx = threadIdx.x; idx < nhere * wn; idx += blockDim.x) {
-    long el = idx / wn; int w = (int)(idx - el * wn);
-    stage[el * pitch + w] = A.min[(base + el) * wn + w];
-  }
-  __syncthreads();
-  const long e = base + threadIdx.x;
-  if (e >= A.count || !mine) return;
-  uint32_t* my = stage + threadIdx.x * pitch;
+// residue -> signed mantissa -> correctly rounded double (encoding.py:81-101); `my` is the element's words in
+// shared memory (modified in place)
+__device__ void decode_one(const CodecArgs& A, uint32_t* my, long e) {
+  const int wn = A.wn;
   int c_max = 0, c_neg = 0;     // compare with max_int and with n - max_int
   for (int i = wn - 1; i >= 0; i--) {
     uint32_t v = my[i];
@@ -164,6 +148,30 @@ __global__ void __launch_bounds__(64) k_decode_f64(CodecArgs A) {
   A.fout[e] = neg ? -val : val;
 }
 
+// generic decode, one thread per element, grid-stride over tiles of blockDim elements; with A.only set it finishes
+// what the wide kernel left (usually nothing: every block returns on the zero count)
+__global__ void __launch_bounds__(64) k_decode_f64(CodecArgs A) {
+  extern __shared__ uint32_t stage[];
+  const int wn = A.wn, pitch = wn + 1;
+  if (A.only && *A.nslow == 0ull) return;
+  for (long base = (long)blockIdx.x * blockDim.x; base < A.count; base += (long)gridDim.x * blockDim.x) {
+    const long nhere = min((long)blockDim.x, A.count - base);
+    const long e = base + threadIdx.x;
+    bool mine = e < A.count;
+    if (A.only) {
+      mine = mine && A.only[e] != 0;
+      if (!__syncthreads_or(mine)) continue;      // nothing in this tile was left to the generic path
+    }
+    for (long idx = threadIdx.x; idx < nhere * wn; idx += blockDim.x) {
+      long el = idx / wn; int w = (int)(idx - el * wn);
+      stage[el * pitch + w] = A.min[(base + el) * wn + w];
+    }
+    __syncthreads();
+    if (mine) decode_one(A, stage + threadIdx.x * pitch, e);
+    __syncthreads();
+  }
+}
+
 
 // ---- HBM-bound forms of the two codec kernels ----------------------------------------------------------------
 //
@@ -174,6 +182,7 @@ __global__ void __launch_bounds__(64) k_decode_f64(CodecArgs A) {
 // and wn >= 8 (the host falls back to the kernels above otherwise).
 
 // encode: pass 1 stores the background (0 or n), pass 2 patches the up-to-three magnitude words and the borrow run
+template <bool TWO>     // TWO: more than 64 words per residue (a second 16-byte column per lane)
 __global__ void __launch_bounds__(256) k_encode_f64_wide(CodecArgs A) {
   const int lane = threadIdx.x & 31;
   const long warp = (long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -237,18 +246,19 @@ __global__ void __launch_bounds__(256) k_encode_f64_wide(CodecArgs A) {
     }
     // pass 1: background, two elements per step, 16 lanes x 16 bytes each
     const uint32_t negmask = __ballot_sync(0xffffffffu, neg);
-    const int half = lane >> 4, l16 = lane & 15;
-    for (int s = 0; s < 32; s += 2) {
-      const int src = s + half;
-      const long ee = eb + src;
-      if (ee < A.count) {
-        const bool isneg = (negmask >> src) & 1u;
-        uint32_t* dst = A.mout + ee * wn;
-        for (int i0 = 4 * l16; i0 < wn; i0 += 64) {
-          uint4 val = make_uint4(0u, 0u, 0u, 0u);
-          if (isneg) val = ld4(A.nwords + i0);
-          *reinterpret_cast<uint4*>(dst + i0) = val;
-        }
+    {
+      const int half = lane >> 4, i0 = 4 * (lane & 15);
+      const bool act0 = i0 < wn, act1 = TWO && i0 + 64 < wn;
+      const uint4 zero4 = make_uint4(0u, 0u, 0u, 0u);
+      const uint4 nv0 = act0 ? ld4(A.nwords + i0) : zero4, nv1 = act1 ? ld4(A.nwords + i0 + 64) : zero4;
+      const bool full = eb + 32 <= A.count;
+      uint32_t* q = A.mout + (eb + half) * (long)wn + i0;
+#pragma unroll
+      for (int s = 0; s < 32; s += 2) {
+        const bool in = full || eb + s + half < A.count;
+        const bool isneg = (negmask >> (s + half)) & 1u;
+        if (act0 && in) *reinterpret_cast<uint4*>(q + (long)s * wn) = isneg ? nv0 : zero4;
+        if (TWO && act1 && in) *reinterpret_cast<uint4*>(q + (long)s * wn + 64) = isneg ? nv1 : zero4;
       }
     }
     __syncwarp();
@@ -270,16 +280,17 @@ __global__ void __launch_bounds__(256) k_encode_f64_wide(CodecArgs A) {
 // decode: pass 1 checks that every word from the fourth up is background (all zero, or all equal to n); pass 2
 // turns the low 96 bits into the correctly rounded double.  Anything else -- wide magnitudes, the overflow band --
 // is marked in A.slow for the generic kernel.  Needs max_int >= 2^96 (maxint_top >= 3).
+template <bool TWO>
 __global__ void __launch_bounds__(256, 4) k_decode_f64_wide(CodecArgs A) {
   const int lane = threadIdx.x & 31;
   const long warp = (long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const long nwarps = (long)gridDim.x * (blockDim.x >> 5);
   const int wn = A.wn;
-  const int half = lane >> 4, l16 = lane & 15;
-  const int i0 = 4 * l16;
-  uint4 nv0 = make_uint4(0u, 0u, 0u, 0u), nv1 = nv0;             // this lane's words of n (chunks 0 and 1)
-  if (i0 < wn) nv0 = ld4(A.nwords + i0);
-  if (i0 + 64 < wn) nv1 = ld4(A.nwords + i0 + 64);
+  const int half = lane >> 4, l16 = lane & 15, i0 = 4 * l16;
+  const bool act0 = i0 < wn, act1 = TWO && i0 + 64 < wn;
+  const uint4 zero4 = make_uint4(0u, 0u, 0u, 0u);
+  const uint4 nv0 = act0 ? ld4(A.nwords + i0) : zero4, nv1 = act1 ? ld4(A.nwords + i0 + 64) : zero4;
+  const uint32_t low3 = l16 ? 0xffffffffu : 0u;          // lane 0 of an element ignores its words 0..2
   for (long eb = warp * 32; eb < A.count; eb += nwarps * 32) {
     // own element's low words first: their latency hides behind pass 1
     const long e = eb + lane;
@@ -288,41 +299,34 @@ __global__ void __launch_bounds__(256, 4) k_decode_f64_wide(CodecArgs A) {
       const uint32_t* x = A.min + e * wn;
       m0 = x[0]; m1 = x[1]; m2 = x[2];
     }
-    bool my_zero = false, my_n = false;
-    for (int s = 0; s < 32; s += 8) {                             // four steps of two elements, loads issued together
+    const bool full = eb + 32 <= A.count;
+    const uint32_t* p = A.min + (eb + half) * (long)wn + i0;
+    uint32_t zbits = 0, nbits = 0;        // bit k: every word from the fourth up of element eb + k is 0 / equals n
+#pragma unroll 1
+    for (int s = 0; s < 32; s += 8) {     // four steps of two elements, loads issued together
       uint4 xa[4], xb[4];
-      bool in[4];
 #pragma unroll
       for (int j = 0; j < 4; j++) {
-        const long ee = eb + s + 2 * j + half;
-        in[j] = ee < A.count;
-        xa[j] = nv0;
-        xb[j] = nv1;
-        if (in[j] && i0 < wn) xa[j] = ld4(A.min + ee * wn + i0);
-        if (in[j] && i0 + 64 < wn) xb[j] = ld4(A.min + ee * wn + i0 + 64);
+        const bool in = full || eb + s + 2 * j + half < A.count;
+        xa[j] = (act0 && in) ? ld4(p + (long)(s + 2 * j) * wn) : nv0;
+        xb[j] = (TWO && act1 && in) ? ld4(p + (long)(s + 2 * j) * wn + 64) : nv1;
       }
 #pragma unroll
       for (int j = 0; j < 4; j++) {
-        bool zero_ok = true, n_ok = true;
-        if (in[j] && i0 < wn) {
-          if (i0 == 0) {
-            zero_ok = xa[j].w == 0u;
-            n_ok = xa[j].w == nv0.w;
-          } else {
-            zero_ok = (xa[j].x | xa[j].y | xa[j].z | xa[j].w) == 0u;
-            n_ok = xa[j].x == nv0.x && xa[j].y == nv0.y && xa[j].z == nv0.z && xa[j].w == nv0.w;
-          }
+        uint32_t z = ((xa[j].x | xa[j].y | xa[j].z) & low3) | xa[j].w;
+        uint32_t d = (((xa[j].x ^ nv0.x) | (xa[j].y ^ nv0.y) | (xa[j].z ^ nv0.z)) & low3) | (xa[j].w ^ nv0.w);
+        if (TWO) {
+          z |= xb[j].x | xb[j].y | xb[j].z | xb[j].w;
+          d |= (xb[j].x ^ nv1.x) | (xb[j].y ^ nv1.y) | (xb[j].z ^ nv1.z) | (xb[j].w ^ nv1.w);
         }
-        if (in[j] && i0 + 64 < wn) {
-          zero_ok &= (xb[j].x | xb[j].y | xb[j].z | xb[j].w) == 0u;
-          n_ok &= xb[j].x == nv1.x && xb[j].y == nv1.y && xb[j].z == nv1.z && xb[j].w == nv1.w;
-        }
-        const uint32_t bz = __ballot_sync(0xffffffffu, zero_ok), bn = __ballot_sync(0xffffffffu, n_ok);
+        // inactive lanes hold n's (zero) words: they vote "equal to n" and, being zero, "zero" as well
+        const uint32_t bz = __ballot_sync(0xffffffffu, z == 0u), bn = __ballot_sync(0xffffffffu, d == 0u);
         const int first = s + 2 * j;
-        if (lane == first) { my_zero = (bz & 0xffffu) == 0xffffu; my_n = (bn & 0xffffu) == 0xffffu; }
-        if (lane == first + 1) { my_zero = (bz >> 16) == 0xffffu; my_n = (bn >> 16) == 0xffffu; }
+        zbits |= ((uint32_t)((bz & 0xffffu) == 0xffffu) << first) | ((uint32_t)((bz >> 16) == 0xffffu) << (first + 1));
+        nbits |= ((uint32_t)((bn & 0xffffu) == 0xffffu) << first) | ((uint32_t)((bn >> 16) == 0xffffu) << (first + 1));
       }
     }
+    const bool my_zero = (zbits >> lane) & 1u, my_n = (nbits >> lane) & 1u;
     if (e >= A.count) continue;
     bool neg = false, slow = false;
     if (my_zero) {
@@ -476,10 +480,11 @@ int hb_encode_f64(hb_ctx* ctx, const double* values, int exponent, uint32_t* m_o
   A.negband = ctx->d_pub + ctx->off_negband; A.wn = ctx->wn; A.exponent = exponent; A.count = count;
   A.fin = values; A.mout = m_out; A.first_bad = (unsigned long long*)first_bad;
   A.maxint_top = ctx->maxint_top;
-  if (ctx->wn % 4 == 0 && ctx->wn >= 8) {
+  if (ctx->wn % 4 == 0 && ctx->wn >= 8 && ctx->wn <= 128) {
     const long warps = (count + 31) / 32;
     const long blocks = std::min<long>((warps + 7) / 8, (long)ctx->sms * 8);
-    hb::k_encode_f64_wide<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream_>>>(A);
+    if (ctx->wn > 64) hb::k_encode_f64_wide<true><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream_>>>(A);
+    else hb::k_encode_f64_wide<false><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream_>>>(A);
   } else {
     const int threads = 64;
     const size_t smem = (size_t)threads * (ctx->wn + 1) * sizeof(uint32_t);
@@ -518,13 +523,15 @@ int hb_decode_f64(hb_ctx* ctx, const uint32_t* m, int exponent, double* values_o
     CU(cudaMemsetAsync(ctx->codec_scratch, 0, 8, stream));
     const long warps = (count + 31) / 32;
     const long blocks = std::min<long>((warps + 7) / 8, (long)ctx->sms * 4);
-    hb::k_decode_f64_wide<<<(unsigned)blocks, 256, 0, stream>>>(A);
+    if (ctx->wn > 64) hb::k_decode_f64_wide<true><<<(unsigned)blocks, 256, 0, stream>>>(A);
+    else hb::k_decode_f64_wide<false><<<(unsigned)blocks, 256, 0, stream>>>(A);
     g_launches++;
     A.only = slow;
   }
   const int threads = 64;
   const size_t smem = (size_t)threads * (ctx->wn + 1) * sizeof(uint32_t);
-  hb::k_decode_f64<<<(unsigned)((count + threads - 1) / threads), threads, smem, stream>>>(A);
+  const long tiles = (count + threads - 1) / threads;
+  hb::k_decode_f64<<<(unsigned)std::min<long>(tiles, (long)ctx->sms * 16), threads, smem, stream>>>(A);
   g_launches++;
   CU(cudaGetLastError());
   return HB_OK;
