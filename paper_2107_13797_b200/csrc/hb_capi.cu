@@ -13,8 +13,14 @@ std::atomic<long long> g_launches{0};
 
 namespace {
 
+// Words of window-table scratch a launch of `count` elements needs (per-warp tiles, see hb_kernels.cuh).
+size_t table_words(const hb_ctx* ctx, int base_cfg, int slots, int64_t count) {
+  Launch l = plan(ctx, base_cfg, count);
+  return (size_t)(slots + 1) * kCfgs[l.cfg].lpt * 32 * l.nwarps;
+}
+
 int encrypt_common(hb_ctx* ctx, const uint32_t* m, const uint32_t* c, const uint32_t* r, uint32_t* out,
-                   int64_t count, int mode, void* stream_) {
+                   int64_t count, int mode, void* stream_, uint32_t* tbl_ext = nullptr) {
   if (!ctx || !r || !out || (mode == 0 ? !m : !c)) return fail(HB_ERR_ARG, "null pointer");
   if (count < 0) return fail(HB_ERR_ARG, "negative count");
   if (count == 0) return HB_OK;
@@ -23,8 +29,8 @@ int encrypt_common(hb_ctx* ctx, const uint32_t* m, const uint32_t* c, const uint
   const int cfg = ctx->cfg_pub;
   Launch l = plan(ctx, cfg, count);
   const long stride = (long)(ctx->slots_n + 1) * kCfgs[l.cfg].lpt * 32;
-  uint32_t* tbl = nullptr;
-  CU(cudaMallocAsync(&tbl, (size_t)stride * l.nwarps * sizeof(uint32_t), stream));
+  uint32_t* tbl = tbl_ext;
+  if (!tbl) CU(cudaMallocAsync(&tbl, (size_t)stride * l.nwarps * sizeof(uint32_t), stream));
   hb::EncArgs A;
   A.mod = dev_mod(ctx->d_pub, ctx->mod_n2);
   A.nR = ctx->d_pub + ctx->off_nR;
@@ -36,7 +42,7 @@ int encrypt_common(hb_ctx* ctx, const uint32_t* m, const uint32_t* c, const uint
   A.count = count; A.wn = ctx->wn; A.wc = ctx->wc; A.mode = mode;
   HB_DISPATCH_POW(cfg, k_encrypt, l, stream, A)
   CU(cudaGetLastError());
-  CU(cudaFreeAsync(tbl, stream));
+  if (!tbl_ext) CU(cudaFreeAsync(tbl, stream));
   return HB_OK;
 }
 
@@ -75,6 +81,16 @@ int hb_ctx_create(hb_ctx** out, const uint32_t* n_words, int n_nwords, int devic
   CU(cudaGetDeviceCount(&ndev));
   if (device < 0 || device >= ndev) return fail(HB_ERR_CUDA, "no such CUDA device");
   CU(cudaSetDevice(device));
+  {
+    // every operator takes its scratch from the stream-ordered allocator; keep freed blocks in the pool instead of
+    // handing them back to the driver at each synchronisation (the default release threshold is zero)
+    cudaMemPool_t pool = nullptr;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess && pool) {
+      unsigned long long keep = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
+  }
   hb_ctx* ctx = new hb_ctx();
   ctx->device = device;
   cudaDeviceProp prop;
@@ -177,9 +193,12 @@ int hb_ctx_set_private(hb_ctx* ctx, const uint32_t* p_, const uint32_t* q_, cons
   return HB_OK;
 }
 
+static void release_stages(hb_ctx* ctx);
+
 void hb_ctx_destroy(hb_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
+  release_stages(ctx);
   if (ctx->d_pub) cudaFree(ctx->d_pub);
   if (ctx->d_priv) cudaFree(ctx->d_priv);
   if (ctx->codec_scratch) cudaFree(ctx->codec_scratch);
@@ -252,7 +271,8 @@ int hb_sqrmod(hb_ctx* ctx, const uint32_t* a, uint32_t* out, int64_t count, int 
   return HB_OK;
 }
 
-int hb_decrypt(hb_ctx* ctx, const uint32_t* c, uint32_t* m_out, int64_t count, void* stream_) {
+static int decrypt_common(hb_ctx* ctx, const uint32_t* c, uint32_t* m_out, int64_t count, void* stream_,
+                          uint32_t* tbl_ext) {
   if (!ctx || !c || !m_out) return fail(HB_ERR_ARG, "null pointer");
   if (!ctx->has_private) return fail(HB_ERR_NOPRIVATE, "context has no private key");
   if (count < 0) return fail(HB_ERR_ARG, "negative count");
@@ -262,8 +282,8 @@ int hb_decrypt(hb_ctx* ctx, const uint32_t* c, uint32_t* m_out, int64_t count, v
   const int cfg = ctx->cfg_priv;
   Launch l = plan(ctx, cfg, count);
   const long stride = (long)(ctx->slots_priv + 1) * kCfgs[l.cfg].lpt * 32;
-  uint32_t* tbl = nullptr;
-  CU(cudaMallocAsync(&tbl, (size_t)stride * l.nwarps * sizeof(uint32_t), stream));
+  uint32_t* tbl = tbl_ext;
+  if (!tbl) CU(cudaMallocAsync(&tbl, (size_t)stride * l.nwarps * sizeof(uint32_t), stream));
   const uint32_t* base = ctx->d_priv;
   hb::DecArgs A;
   for (int h = 0; h < 2; h++) {
@@ -281,19 +301,43 @@ int hb_decrypt(hb_ctx* ctx, const uint32_t* c, uint32_t* m_out, int64_t count, v
   A.c = c; A.out = m_out; A.count = count; A.wn = ctx->wn; A.wc = ctx->wc;
   HB_DISPATCH_POW(cfg, k_decrypt, l, stream, A)
   CU(cudaGetLastError());
-  CU(cudaFreeAsync(tbl, stream));
+  if (!tbl_ext) CU(cudaFreeAsync(tbl, stream));
   return HB_OK;
 }
 
+int hb_decrypt(hb_ctx* ctx, const uint32_t* c, uint32_t* m_out, int64_t count, void* stream) {
+  return decrypt_common(ctx, c, m_out, count, stream, nullptr);
+}
+
 // ---- host-buffer path: pinned staging + two side streams, chunks double-buffered ------------------
-namespace {
-struct Stage {
-  cudaStream_t s = nullptr;
-  uint32_t *h_in0 = nullptr, *h_in1 = nullptr, *h_out = nullptr;
-  uint32_t *d_in0 = nullptr, *d_in1 = nullptr, *d_out = nullptr;
-  cudaEvent_t done = nullptr;
-};
-}  // namespace
+// The stages live in the context and only ever grow, so a warm call allocates nothing: pinned allocations cost
+// milliseconds each, and a stream-ordered allocation of the 80 MB window-table scratch per chunk on alternating
+// streams defeats the pool's reuse.
+static int grow(void** p, size_t* cap, size_t need, bool pinned) {
+  if (*cap >= need) return HB_OK;
+  if (*p) { if (pinned) cudaFreeHost(*p); else cudaFree(*p); *p = nullptr; *cap = 0; }
+  const size_t want = need + need / 8;
+  cudaError_t e = pinned ? cudaMallocHost(p, want) : cudaMalloc(p, want);
+  if (e != cudaSuccess) return fail(HB_ERR_CUDA, std::string("staging allocation: ") + cudaGetErrorString(e));
+  *cap = want;
+  return HB_OK;
+}
+
+static void release_stages(hb_ctx* ctx) {
+  for (auto& s : ctx->stage) {
+    if (s.s) cudaStreamSynchronize(s.s);
+    if (s.h_in0) cudaFreeHost(s.h_in0);
+    if (s.h_in1) cudaFreeHost(s.h_in1);
+    if (s.h_out) cudaFreeHost(s.h_out);
+    if (s.d_in0) cudaFree(s.d_in0);
+    if (s.d_in1) cudaFree(s.d_in1);
+    if (s.d_out) cudaFree(s.d_out);
+    if (s.d_tbl) cudaFree(s.d_tbl);
+    if (s.done) cudaEventDestroy(s.done);
+    if (s.s) cudaStreamDestroy(s.s);
+    s = hb_ctx::HostStage();
+  }
+}
 
 static int host_pipeline(hb_ctx* ctx, int kind, const uint32_t* in0, const uint32_t* in1, uint32_t* out,
                          int64_t count) {
@@ -306,41 +350,36 @@ static int host_pipeline(hb_ctx* ctx, int kind, const uint32_t* in0, const uint3
   const size_t w_out = kind == 0 ? ctx->wc : ctx->wn;
   const int cfg = kind == 0 ? ctx->cfg_pub : ctx->cfg_priv;
   if (cfg < 0) return fail(HB_ERR_NOPRIVATE, "context has no private key");
+  const int slots = kind == 0 ? ctx->slots_n : ctx->slots_priv;
   // four full waves of the persistent grid per chunk, so chunking costs no tail
   const int64_t wave = (int64_t)ctx->sms * 4 * hb::blocks_per_sm(kCfgs[cfg].lpt) * (32 / kCfgs[cfg].tpi);
   const int64_t chunk = std::min<int64_t>(count, 4 * wave);
-  Stage st[2];
-  int rc = HB_OK;
-  auto cleanup = [&]() {
-    for (auto& s : st) {
-      if (s.s) cudaStreamSynchronize(s.s);
-      if (s.h_in0) cudaFreeHost(s.h_in0);
-      if (s.h_in1) cudaFreeHost(s.h_in1);
-      if (s.h_out) cudaFreeHost(s.h_out);
-      if (s.d_in0) cudaFree(s.d_in0);
-      if (s.d_in1) cudaFree(s.d_in1);
-      if (s.d_out) cudaFree(s.d_out);
-      if (s.done) cudaEventDestroy(s.done);
-      if (s.s) cudaStreamDestroy(s.s);
-    }
-  };
-#define CUX(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { cleanup(); \
-  return fail(HB_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); } } while (0)
   const int nst = count > chunk ? 2 : 1;
-  for (int i = 0; i < nst; i++) {
-    CUX(cudaStreamCreateWithFlags(&st[i].s, cudaStreamNonBlocking));
-    CUX(cudaEventCreateWithFlags(&st[i].done, cudaEventDisableTiming));
-    CUX(cudaMallocHost(&st[i].h_in0, chunk * w_in0 * 4));
-    CUX(cudaMalloc(&st[i].d_in0, chunk * w_in0 * 4));
-    if (w_in1) { CUX(cudaMallocHost(&st[i].h_in1, chunk * w_in1 * 4)); CUX(cudaMalloc(&st[i].d_in1, chunk * w_in1 * 4)); }
-    CUX(cudaMallocHost(&st[i].h_out, chunk * w_out * 4));
-    CUX(cudaMalloc(&st[i].d_out, chunk * w_out * 4));
-  }
-  struct Pending { int64_t off, n; bool active; } pend[2] = {{0, 0, false}, {0, 0, false}};
   const int64_t nchunks = (count + chunk - 1) / chunk;
+  const int64_t last = count - (nchunks - 1) * chunk;
+  const size_t tbl_bytes =
+      sizeof(uint32_t) * std::max(table_words(ctx, cfg, slots, chunk), table_words(ctx, cfg, slots, last));
+  for (int i = 0; i < nst; i++) {
+    hb_ctx::HostStage& s = ctx->stage[i];
+    if (!s.s) CU(cudaStreamCreateWithFlags(&s.s, cudaStreamNonBlocking));
+    if (!s.done) CU(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming));
+    CU(cudaStreamSynchronize(s.s));
+    int rc = grow((void**)&s.h_in0, &s.hcap_in0, chunk * w_in0 * 4, true);
+    if (!rc) rc = grow((void**)&s.d_in0, &s.dcap_in0, chunk * w_in0 * 4, false);
+    if (!rc && w_in1) rc = grow((void**)&s.h_in1, &s.hcap_in1, chunk * w_in1 * 4, true);
+    if (!rc && w_in1) rc = grow((void**)&s.d_in1, &s.dcap_in1, chunk * w_in1 * 4, false);
+    if (!rc) rc = grow((void**)&s.h_out, &s.hcap_out, chunk * w_out * 4, true);
+    if (!rc) rc = grow((void**)&s.d_out, &s.dcap_out, chunk * w_out * 4, false);
+    if (!rc) rc = grow((void**)&s.d_tbl, &s.dcap_tbl, tbl_bytes, false);
+    if (rc) return rc;
+  }
+  auto drain = [&]() { for (int i = 0; i < nst; i++) cudaStreamSynchronize(ctx->stage[i].s); };
+#define CUX(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { drain(); \
+  return fail(HB_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); } } while (0)
+  struct Pending { int64_t off, n; bool active; } pend[2] = {{0, 0, false}, {0, 0, false}};
   for (int64_t i = 0; i < nchunks + nst; i++) {
     const int which = (int)(i % nst);
-    Stage& s = st[which];
+    hb_ctx::HostStage& s = ctx->stage[which];
     if (pend[which].active) {   // drain the chunk this stage submitted nst iterations ago
       CUX(cudaEventSynchronize(s.done));
       memcpy(out + pend[which].off * w_out, s.h_out, pend[which].n * w_out * 4);
@@ -354,14 +393,14 @@ static int host_pipeline(hb_ctx* ctx, int kind, const uint32_t* in0, const uint3
       memcpy(s.h_in1, in1 + off * w_in1, n * w_in1 * 4);
       CUX(cudaMemcpyAsync(s.d_in1, s.h_in1, n * w_in1 * 4, cudaMemcpyHostToDevice, s.s));
     }
-    rc = kind == 0 ? hb_encrypt(ctx, s.d_in0, s.d_in1, s.d_out, n, s.s) : hb_decrypt(ctx, s.d_in0, s.d_out, n, s.s);
-    if (rc != HB_OK) { cleanup(); return rc; }
+    const int rc = kind == 0 ? encrypt_common(ctx, s.d_in0, nullptr, s.d_in1, s.d_out, n, 0, s.s, s.d_tbl)
+                             : decrypt_common(ctx, s.d_in0, s.d_out, n, s.s, s.d_tbl);
+    if (rc != HB_OK) { drain(); return rc; }
     CUX(cudaMemcpyAsync(s.h_out, s.d_out, n * w_out * 4, cudaMemcpyDeviceToHost, s.s));
     CUX(cudaEventRecord(s.done, s.s));
     pend[which] = {off, n, true};
   }
 #undef CUX
-  cleanup();
   return HB_OK;
 }
 

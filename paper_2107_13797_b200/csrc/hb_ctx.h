@@ -120,8 +120,17 @@ struct hb_ctx {
   size_t off_qinvR = 0, off_qR = 0;
   hbi::ModOff mod_n_priv;
   int slots_priv = 0;
-  // host-path staging
+  // host-path staging (hb_encrypt_host / hb_decrypt_host): two stages of pinned + device buffers and window-table
+  // scratch, kept across calls (grow-only) so a call costs no allocation once warm
   std::mutex mu;
+  struct HostStage {
+    cudaStream_t s = nullptr;
+    cudaEvent_t done = nullptr;
+    uint32_t *h_in0 = nullptr, *h_in1 = nullptr, *h_out = nullptr;
+    uint32_t *d_in0 = nullptr, *d_in1 = nullptr, *d_out = nullptr, *d_tbl = nullptr;
+    size_t hcap_in0 = 0, hcap_in1 = 0, hcap_out = 0;                 // bytes, pinned side
+    size_t dcap_in0 = 0, dcap_in1 = 0, dcap_out = 0, dcap_tbl = 0;   // bytes, device side
+  } stage[2];
 };
 
 namespace hbi {
