@@ -200,7 +200,11 @@ int matvec_ab(hb_ctx* ctx, const uint32_t* c, const PrepOut& pr, long inner, int
   const int cfg = ctx->cfg_pub;
   const int L = Ldig(cfg);
   hb::ModDev mod = dev_mod(ctx->d_pub, ctx->mod_n2);
-  int cbits = inner >= 4096 ? 8 : inner >= 1024 ? 7 : inner >= 256 ? 6 : inner >= 64 ? 5 : inner >= 16 ? 3 : 2;
+  // Window width by row count.  9 bits (1024 buckets per column and window, one window fewer for 52-bit scalars) pays
+  // once the per-window bucket work (about 6 * 2^c multiplications and a 2 * 2^c-step sequential fold) is small next
+  // to the rows; the sorted list packs bucket << 22 | row, so 9 is also the widest that fits with rows < 2^22.
+  int cbits = inner >= 32768 && inner < (1L << 22) ? 9
+            : inner >= 4096 ? 8 : inner >= 1024 ? 7 : inner >= 256 ? 6 : inner >= 64 ? 5 : inner >= 16 ? 3 : 2;
   const int maxbits = std::max(pr.maxbits, 1);
   const int nwin = (maxbits + cbits - 1) / cbits;
   const int NB = 2 << cbits;
