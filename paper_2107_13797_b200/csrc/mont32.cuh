@@ -100,14 +100,16 @@ struct Mont {
   // E, O += v * x : one carry chain per accumulator array (H multiply-adds each)
   __device__ __forceinline__ void mac_row(uint64_t (&E)[H + 1], uint64_t (&O)[H + 1], const uint32_t (&v)[LPT],
                                           uint32_t x) const {
+    // E[H] and O[H] only ever collect chain carries (a handful per row before the frame moves on), so they are
+    // kept as 32-bit counts: one add instead of a 64-bit pair
     E[0] = mac_cc(v[0], x, E[0]);
 #pragma unroll
     for (int i = 1; i < H; i++) E[i] = macc_cc(v[2 * i], x, E[i]);
-    E[H] = addc64(E[H], 0);
+    E[H] = (uint64_t)addc32(lo32(E[H]), 0u);
     O[0] = mac_cc(v[1], x, O[0]);
 #pragma unroll
     for (int i = 1; i < H; i++) O[i] = macc_cc(v[2 * i + 1], x, O[i]);
-    O[H] = addc64(O[H], 0);
+    O[H] = (uint64_t)addc32(lo32(O[H]), 0u);
   }
 
   // Resolves pending single-bit carries between lanes: g (0/1) leaves this lane; returns the carry that
@@ -224,8 +226,8 @@ struct Mont {
         const uint32_t vlo = add_cc32(lo32(E[0]), pend_lo);
         const uint32_t vhi = addc_cc32(hi32(E[0]), pend_hi);
         const uint32_t vtop = addc32(0, 0);
-        uint32_t recv = __shfl_down_sync(FULLMASK, vlo, 1, TPI);
-        recv = top ? 0u : recv;
+        // from the lane above; the top lane wraps to lane 0, whose low word has just been eliminated (it is zero)
+        const uint32_t recv = __shfl_sync(FULLMASK, vlo, t + 1, TPI);
         pend_lo = vhi;
         pend_hi = vtop;
         // frame moves down one column: E <- O, O[k] <- E[k + 1], the received word lands on the top column
@@ -234,8 +236,12 @@ struct Mont {
         for (int k = 0; k <= H; k++) F[k] = O[k];
 #pragma unroll
         for (int k = 0; k < H - 1; k++) O[k] = E[k + 1];
-        O[H - 1] = add_cc64(E[H], (uint64_t)recv);
-        O[H] = addc64(0, 0);
+        {                                     // E[H] is a small count: count + recv fits 33 bits
+          const uint32_t lo = add_cc32(lo32(E[H]), recv);
+          const uint32_t hi = addc32(0u, 0u);
+          O[H - 1] = ((uint64_t)hi << 32) | lo;
+          O[H] = 0;
+        }
 #pragma unroll
         for (int k = 0; k <= H; k++) E[k] = F[k];
       }
@@ -320,8 +326,10 @@ struct Mont {
     for (int k = 0; k <= H; k++) F[k] = O[k];
 #pragma unroll
     for (int k = 0; k < H - 1; k++) O[k] = E[k + 1];
-    O[H - 1] = add_cc64(E[H], (uint64_t)recv);
-    O[H] = addc64(0, 0);
+    const uint32_t lo = add_cc32(lo32(E[H]), recv);        // E[H] is a small count: count + recv fits 33 bits
+    const uint32_t hi = addc32(0u, 0u);
+    O[H - 1] = ((uint64_t)hi << 32) | lo;
+    O[H] = 0;
 #pragma unroll
     for (int k = 0; k <= H; k++) E[k] = F[k];
   }
@@ -348,8 +356,7 @@ struct Mont {
         const uint32_t vlo = add_cc32(lo32(E[0]), pend_lo);
         const uint32_t vhi = addc_cc32(hi32(E[0]), pend_hi);
         const uint32_t vtop = addc32(0, 0);
-        uint32_t recv = __shfl_down_sync(FULLMASK, vlo, 1, TPI);
-        recv = top ? 0u : recv;
+        const uint32_t recv = __shfl_sync(FULLMASK, vlo, t + 1, TPI);    // top lane wraps to lane 0: zero
         pend_lo = vhi;
         pend_hi = vtop;
         frame_down(E, O, recv);
