@@ -449,10 +449,10 @@ def flr_extra(rows: int, features: int = 200):
 
 def _ncu_traffic_per_element():
     """dram bytes read + written per encrypted element, from the committed ncu --set full capture of k_encrypt
-    (profiles/r01c_ncu_summary.json; the capture ran 37888 elements).  Almost all of it is write-back of the
+    (profiles/r01d_ncu_summary.json; the capture ran 37888 elements).  Almost all of it is write-back of the
     per-warp window tables (17 slots x 4 KiB per warp), not operand traffic."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01c_ncu_summary.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", "r01d_ncu_summary.json")) as fh:
             enc = json.load(fh)["encrypt"]
         mb = float(enc["dram__bytes_read.sum"]["value"]) + float(enc["dram__bytes_write.sum"]["value"])
         return mb * 1e6 / 37888
