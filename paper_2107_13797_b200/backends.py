@@ -73,6 +73,66 @@ class CudaBackend(ExecutionBackend):
         _native.check(self.lib().hb_obfuscate(ctx.handle, c.ptr(), r.ptr(), out.ptr(), c.count, self._stream()))
         return out
 
+    # chunk of the streamed encrypt / obfuscate: a whole number of persistent-grid waves for every limb shape
+    # (lcm of 9472, 7104, 18944, 28416 instances per wave, times two)
+    STREAM_CHUNK = 113664
+
+    def encrypt_drawing(self, n: int, src: device.WordArray, rng, obfuscate: bool = False):
+        """batch_encrypt / batch_obfuscate with the obfuscation factors drawn while the GPU works: the native
+        MT19937 replay (draw_units) produces chunk k + 1 on the host while chunk k's modular powers run, the gcd test
+        of every chunk is one product on the device, and the results are looked at once at the end.  Same values in
+        the same order as [draw_unit(n, rng) for each element] (operators.py:133,142 of the reference).  Returns
+        None when the batch does not qualify (small batch, small modulus, a generator that is not exactly
+        random.Random): the caller then takes the one-shot path."""
+        import ctypes
+        import math
+        import random as _random
+        import numpy as np
+        count = src.count
+        if type(rng) is not _random.Random or n.bit_length() < 256 or count < 2 * self.STREAM_CHUNK:
+            return None
+        t = device.torch()
+        ctx = device.context_for(n)
+        lib = self.lib()
+        wn, wc = ctx.wn, ctx.wc
+        w_src = wc if obfuscate else wn
+        saved = rng.getstate()
+        version, internal, gauss = saved
+        state = np.array(internal[:624], dtype=np.uint32)
+        index = ctypes.c_int(internal[624])
+        n_words = device.ints_to_words([n], wn)
+        out = device.WordArray.empty_device(count, wc)
+        chunk = self.STREAM_CHUNK
+        nchunks = (count + chunk - 1) // chunk
+        pinned = [t.empty((chunk, wn), dtype=t.int32, pin_memory=True) for _ in range(2)]
+        staged = [t.empty((chunk, wn), dtype=t.int32, device="cuda") for _ in range(2)]
+        copied = [None, None]
+        checks = t.empty((nchunks, wc), dtype=t.int32, device="cuda")
+        stream = self._stream()
+        src_ptr, out_ptr = src.ptr(), out.ptr()
+        for k in range(nchunks):
+            off = k * chunk
+            cnt = min(chunk, count - off)
+            which = k & 1
+            if copied[which] is not None:
+                copied[which].synchronize()            # the upload that last used this pinned buffer is done
+            host = pinned[which].numpy()
+            _native.check(lib.hb_mt19937_randrange1(state.ctypes.data, ctypes.byref(index), n_words.ctypes.data,
+                                                    wn, cnt, host.ctypes.data))
+            staged[which][:cnt].copy_(pinned[which][:cnt], non_blocking=True)
+            copied[which] = t.cuda.Event()
+            copied[which].record()
+            r_ptr = staged[which].data_ptr()
+            _native.check(lib.hb_unit_product(ctx.handle, r_ptr, checks[k].data_ptr(), cnt, stream))
+            call = lib.hb_obfuscate if obfuscate else lib.hb_encrypt
+            _native.check(call(ctx.handle, src_ptr + off * w_src * 4, r_ptr, out_ptr + off * wc * 4, cnt, stream))
+        products = device.WordArray.from_device(checks).ints()
+        if any(math.gcd(p, n) != 1 for p in products):
+            rng.setstate(saved)                        # a non-unit was drawn: let the caller redo it the exact way
+            return None
+        rng.setstate((version, tuple(int(v) for v in state) + (index.value,), gauss))
+        return out
+
     def decrypt(self, n: int, private, c: device.WordArray) -> device.WordArray:
         """private = (p, q, hp, hq, q_inv)."""
         ctx = device.context_for(n)

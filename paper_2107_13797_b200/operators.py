@@ -96,8 +96,10 @@ def batch_encrypt(pk: PublicKey, plain: PlaintextBatch, rng: random.Random,
     if plain.key != pk:
         raise ValueError("plaintext batch was encoded under a different key")
     be = _cuda(backend)
-    r = _draw_units(pk, plain.count, rng, be)
-    out = be.encrypt(pk.n, plain.words, r) if plain.count else WordArray.from_ints((), ct_width(pk))
+    out = be.encrypt_drawing(pk.n, plain.words, rng) if plain.count else None     # large batches: draws overlap the GPU
+    if out is None:
+        r = _draw_units(pk, plain.count, rng, be)
+        out = be.encrypt(pk.n, plain.words, r) if plain.count else WordArray.from_ints((), ct_width(pk))
     return CiphertextBatch(pk, plain.shape, plain.exponents, out, plain.shared_exponent, obfuscated=True)
 
 
@@ -105,8 +107,10 @@ def batch_obfuscate(pk: PublicKey, cipher: CiphertextBatch, rng: random.Random,
                     backend: ExecutionBackend | None = None) -> CiphertextBatch:
     """operators.py:139-145."""
     be = _cuda(backend)
-    r = _draw_units(pk, cipher.count, rng, be)
-    out = be.obfuscate(pk.n, cipher.words, r) if cipher.count else cipher.words
+    out = be.encrypt_drawing(pk.n, cipher.words, rng, obfuscate=True) if cipher.count else None
+    if out is None:
+        r = _draw_units(pk, cipher.count, rng, be)
+        out = be.obfuscate(pk.n, cipher.words, r) if cipher.count else cipher.words
     return CiphertextBatch(pk, cipher.shape, cipher.exponents, out, cipher.shared_exponent, obfuscated=True)
 
 

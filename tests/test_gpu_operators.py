@@ -520,3 +520,39 @@ def test_codec_wide_kernels_edges(bits):
             if int(edge) >= ok.max_int:
                 with pytest.raises(FixedPointOverflow):
                     ops.batch_encode(pk, [1.0, edge], 0)
+
+
+def test_streamed_encrypt_equals_one_shot(okeys):
+    """Large batches draw their obfuscation factors chunk by chunk while the GPU works (CudaBackend.encrypt_drawing):
+    same ciphertexts, same generator state afterwards as the one-shot path; spot-checked against the oracle."""
+    import numpy as np
+    from paper_2107_13797_b200.device import WordArray
+    ok = okeys("k512")
+    pk, sk = product_keys(ok)
+    be = CudaBackend()
+    count = 2 * be.STREAM_CHUNK + 12345
+    wn = (ok.n.bit_length() + 31) // 32
+    m = np.zeros((count, wn), dtype=np.uint32)
+    m[:, 0] = np.arange(count, dtype=np.uint32) * 2654435761 % (1 << 31)
+    plain = PlaintextBatch(pk, (count,), (-8,), WordArray.from_numpy(m), True)
+    rng_a, rng_b = random.Random(5), random.Random(5)
+    streamed = ops.batch_encrypt(pk, plain, rng_a)                        # takes the streamed path
+    r = be.draw_units(pk.n, count, rng_b)
+    one_shot = be.encrypt(pk.n, plain.words, r)
+    assert np.array_equal(streamed.words.numpy(), one_shot.numpy())
+    assert rng_a.getstate() == rng_b.getstate()
+    rng_c = random.Random(5)
+    picks = [0, 1, be.STREAM_CHUNK - 1, be.STREAM_CHUNK, 2 * be.STREAM_CHUNK, count - 1]
+    rs = [ho.draw_unit(ok.n, rng_c) for _ in range(count)] if count < 300000 else None
+    assert rs is not None
+    want = ho.k_encrypt(ok, [(int(m[i, 0]), rs[i]) for i in picks])
+    got = WordArray.from_numpy(streamed.words.numpy()[picks]).ints()
+    assert list(got) == want
+    # obfuscate streams the same way
+    rng_d, rng_e = random.Random(9), random.Random(9)
+    again = ops.batch_obfuscate(pk, streamed, rng_d)
+    r2 = be.draw_units(pk.n, count, rng_e)
+    assert np.array_equal(again.words.numpy(), be.obfuscate(pk.n, streamed.words, r2).numpy())
+    assert rng_d.getstate() == rng_e.getstate()
+    dec = ops.batch_decrypt(sk, again)
+    assert np.array_equal(dec.words.numpy()[:, 0], m[:, 0])
