@@ -89,12 +89,23 @@ class WordArray:
     def on_device(self) -> bool:
         return self._dev is not None
 
+    @property
+    def on_host(self) -> bool:
+        return self._np is not None or self._ints is not None
+
     def device(self):
         """torch int32 tensor [count, width] on the current CUDA device (uploaded once, then cached)."""
         if self._dev is None:
             require_cuda()
             t = torch()
-            host = t.from_numpy(self.numpy().view(np.int32))
+            arr = self.numpy().view(np.int32)
+            if arr.flags.writeable:
+                host = t.from_numpy(arr)
+            else:                                  # a view of received wire bytes: read-only is what we want
+                import warnings
+                with warnings.catch_warnings():
+                    warnings.simplefilter("ignore")
+                    host = t.from_numpy(arr)
             self._dev = host.cuda(non_blocking=False)
         return self._dev
 

@@ -556,3 +556,29 @@ def test_streamed_encrypt_equals_one_shot(okeys):
     assert rng_d.getstate() == rng_e.getstate()
     dec = ops.batch_decrypt(sk, again)
     assert np.array_equal(dec.words.numpy()[:, 0], m[:, 0])
+
+
+def test_wire_fast_paths(okeys):
+    """HAFB bytes of a large device-resident batch (payload by DMA into pinned staging) equal the bytes of the same
+    batch serialised from host words; deserialising them gives the batch back without a padding copy."""
+    import numpy as np
+    from paper_2107_13797_b200.bufferpool import deserialize, serialize_to_bytes
+    from paper_2107_13797_b200.device import WordArray
+    for name in ("k1024", "k2048"):
+        ok = okeys(name)
+        pk, _ = product_keys(ok)
+        count = 5000
+        wc = ((2 * ok.n.bit_length() + 7) // 8 + 3) // 4
+        rng = np.random.default_rng(3)
+        words = rng.integers(0, 1 << 32, size=(count, wc), dtype=np.uint64).astype(np.uint32)
+        words[:, wc - 1] >>= 2                                     # below n^2
+        host_batch = CiphertextBatch(pk, (count,), (-8,), WordArray.from_numpy(words), True, True)
+        dev_batch = ops.batch_add(pk, host_batch, CiphertextBatch(pk, (count,), (-8,), (1,) * count, True, False))
+        assert dev_batch.words.on_device and not dev_batch.words.on_host
+        fast = serialize_to_bytes(dev_batch)
+        assert not dev_batch.words.on_host                         # no host copy was cached on the way
+        slow = serialize_to_bytes(CiphertextBatch(pk, (count,), (-8,), WordArray.from_numpy(words), True, True))
+        assert fast == slow
+        back = deserialize(fast, pk)
+        assert back == host_batch and back.obfuscated
+        assert ops.batch_add(pk, back, back) == ops.batch_add(pk, host_batch, host_batch)
