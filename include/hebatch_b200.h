@@ -72,6 +72,11 @@ int hb_mulmod(hb_ctx* ctx, const uint32_t* a, const uint32_t* b, uint32_t* out, 
 int hb_lift_mulmod(hb_ctx* ctx, const uint32_t* a, const uint32_t* m, uint32_t* out, int64_t count,
                    int m_broadcast, void* stream);
 
+/* Default exponent of encode_batch (batches.py:122-123): min over the values of encoding.exact_exponent
+ * (encoding.py:44-51), zeros counting as 0.  min_out: device int preset by the caller to INT_MAX (left untouched
+ * only when count == 0). */
+int hb_min_exact_exponent(hb_ctx* ctx, const double* values, int64_t count, int* min_out, void* stream);
+
 /* Plaintext-side residue arithmetic mod n (batches.py:160-205 of the reference).  plain_mul: out[i] = a[i] * b[i]
  * mod n (b_broadcast != 0 uses b[0]); plain_add: out[i] = a[i] + b[i] mod n; plain_rescale
  * (encoding.py:104-113): the signed mantissa times 16^digits, back as a residue -- first_bad (device int64,

@@ -51,6 +51,7 @@ SIGNATURES = {
     "hb_plain_mulmod": (_int, [_vp, _vp, _vp, _vp, _i64, _int, _vp]),
     "hb_plain_addmod": (_int, [_vp, _vp, _vp, _vp, _i64, _vp]),
     "hb_plain_rescale": (_int, [_vp, _vp, _int, _vp, _i64, _vp, _vp]),
+    "hb_min_exact_exponent": (_int, [_vp, _vp, _i64, _vp, _vp]),
     "hb_powscalar": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _int, _vp]),
     "hb_product": (_int, [_vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp]),
     "hb_unit_product": (_int, [_vp, _vp, _vp, _i64, _vp]),

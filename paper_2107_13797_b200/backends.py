@@ -263,8 +263,10 @@ class CudaBackend(ExecutionBackend):
         _native.check(self.lib().hb_matvec_combine(ctx.handle, ab_all.ptr(), nranks, out.ptr(), d, self._stream()))
         return out
 
-    def encode_f64(self, n: int, values, exponent: int) -> device.WordArray:
-        """values: float64 numpy array (host).  Raises FixedPointOverflow like encoding.encode."""
+    def encode_f64(self, n: int, values, exponent) -> device.WordArray:
+        """values: float64 numpy array (host).  exponent None = the batch's exact shared exponent (min of
+        encoding.exact_exponent over the values, batches.py:122-123), computed on the device from the same upload;
+        the exponent used is left in `self.last_exponent`.  Raises FixedPointOverflow like encoding.encode."""
         import numpy as np
         from .encoding import FixedPointOverflow
         ctx = device.context_for(n)
@@ -273,6 +275,14 @@ class CudaBackend(ExecutionBackend):
         if not np.all(np.isfinite(vals)):
             raise ValueError("cannot encode non-finite values")
         dv = t.from_numpy(vals).cuda()
+        if exponent is None:
+            lowest = t.full((1,), 2 ** 31 - 1, dtype=t.int32, device="cuda")
+            _native.check(self.lib().hb_min_exact_exponent(ctx.handle, dv.data_ptr(), vals.shape[0], lowest.data_ptr(),
+                                                           self._stream()))
+            exponent = int(lowest.item())
+            if exponent == 2 ** 31 - 1:
+                exponent = 0
+        self.last_exponent = int(exponent)
         out = device.WordArray.empty_device(vals.shape[0], ctx.wn)
         bad = t.full((1,), -1, dtype=t.int64, device="cuda")
         _native.check(self.lib().hb_encode_f64(ctx.handle, dv.data_ptr(), int(exponent), out.ptr(),

@@ -181,10 +181,10 @@ def encode_batch(pk: PublicKey, values, shape=None, target_exponent: int | None 
     flat, inferred = _flatten(values)
     if shape is None:
         shape = inferred
-    if target_exponent is None:
-        target_exponent = int(encoding.exact_exponents(flat).min()) if flat.size else 0
-    plain = operators.batch_encode(pk, flat, target_exponent)
-    return PlaintextBatch(pk, tuple(shape), (target_exponent,), plain.words, True)
+    if target_exponent is None and flat.size == 0:
+        target_exponent = 0
+    plain = operators.batch_encode(pk, flat, target_exponent)      # None: the exact shared exponent, found on the device
+    return PlaintextBatch(pk, tuple(shape), plain.exponents, plain.words, True)
 
 
 def decode_batch(pk: PublicKey, batch: PlaintextBatch) -> list:

@@ -374,6 +374,24 @@ __global__ void __launch_bounds__(256, 4) k_decode_f64_wide(CodecArgs A) {
   }
 }
 
+// min over the batch of exact_exponent(v) (encoding.py:44-51, batches.py:122-123): the largest base-16 exponent at
+// which every value has an integer mantissa; zeros count as exponent 0.  One atomicMin per warp.
+__global__ void __launch_bounds__(256) k_min_exact_exponent(const double* __restrict__ v, long count, int* out) {
+  int best = 0x7fffffff;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (long)gridDim.x * blockDim.x) {
+    const unsigned long long bits = (unsigned long long)__double_as_longlong(v[i]);
+    const int e11 = (int)((bits >> 52) & 0x7ff);
+    unsigned long long mant = bits & 0xfffffffffffffull;
+    int e2;
+    if (e11 == 0) e2 = -1074; else { mant |= 1ull << 52; e2 = e11 - 1075; }
+    const int ex = mant ? (e2 + (__ffsll((long long)mant) - 1)) >> 2 : 0;      // arithmetic shift = floor division by 4
+    best = min(best, ex);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0 && best != 0x7fffffff) atomicMin(out, best);
+}
+
 // Exact re-grid onto a finer exponent (encoding.py:104-113): signed mantissa times 16^digits, range-checked
 // against max_int, stored back as a residue.  first_bad receives the smallest index that is in the overflow band
 // or overflows after scaling (the host re-examines that element to raise the reference's error).
@@ -450,6 +468,18 @@ __global__ void __launch_bounds__(64) k_plain_rescale(CodecArgs A) {
 }  // namespace hb
 
 extern "C" {
+
+int hb_min_exact_exponent(hb_ctx* ctx, const double* values, int64_t count, int* min_out, void* stream_) {
+  if (!ctx || !values || !min_out) return fail(HB_ERR_ARG, "null pointer");
+  if (count < 0) return fail(HB_ERR_ARG, "negative count");
+  if (count == 0) return HB_OK;
+  CU(cudaSetDevice(ctx->device));
+  const long blocks = std::min<long>((count + 255) / 256, (long)ctx->sms * 8);
+  hb::k_min_exact_exponent<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream_>>>(values, count, min_out);
+  g_launches++;
+  CU(cudaGetLastError());
+  return HB_OK;
+}
 
 int hb_plain_rescale(hb_ctx* ctx, const uint32_t* m, int digits, uint32_t* m_out, int64_t count,
                      int64_t* first_bad, void* stream_) {

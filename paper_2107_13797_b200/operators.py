@@ -75,9 +75,10 @@ def batch_encode(pk: PublicKey, values, exponent: int, backend: ExecutionBackend
     vals = values if isinstance(values, np.ndarray) else np.asarray(list(values), dtype=np.float64)
     vals = np.ascontiguousarray(vals, dtype=np.float64).ravel()
     if vals.shape[0] == 0:
-        return PlaintextBatch(pk, (0,), (exponent,), (), True)
-    words = _cuda(backend).encode_f64(pk.n, vals, exponent)
-    return PlaintextBatch(pk, (vals.shape[0],), (exponent,), words, True)
+        return PlaintextBatch(pk, (0,), (exponent or 0,), (), True)
+    be = _cuda(backend)
+    words = be.encode_f64(pk.n, vals, exponent)        # exponent None (used by encode_batch): exact shared exponent
+    return PlaintextBatch(pk, (vals.shape[0],), (be.last_exponent,), words, True)
 
 
 def batch_decode(pk: PublicKey, batch: PlaintextBatch, backend: ExecutionBackend | None = None) -> list:

@@ -582,3 +582,31 @@ def test_wire_fast_paths(okeys):
         back = deserialize(fast, pk)
         assert back == host_batch and back.obfuscated
         assert ops.batch_add(pk, back, back) == ops.batch_add(pk, host_batch, host_batch)
+
+
+def test_default_exponent_found_on_the_device(okeys):
+    """encode_batch without a target exponent: min over the values of exact_exponent, zeros counting as 0
+    (reference batches.py:122-123), computed by k_min_exact_exponent."""
+    import numpy as np
+    ok = okeys("k1024")
+    pk, _ = product_keys(ok)
+    rng = random.Random(21)
+    cases = [[0.0, 4096.0], [4096.0, 65536.0], [0.0, 0.0, -0.0], [5e-324, 1.0], [2.0 ** -1074 * 3, 2.0 ** 40],
+             [1.0], [0.5], [-0.75, 3.0], [16.0 ** 7, 16.0 ** 9 * 3], [1e-310, 2.5],
+             [rng.uniform(-1, 1) for _ in range(1000)], [float(rng.randrange(1, 1 << 20)) * 16.0 ** 3 for _ in range(300)]]
+    from paper_2107_13797_b200.encoding import FixedPointOverflow
+    for vals in cases:
+        want = min(ho.exact_exponent(v) for v in vals)
+        try:
+            mantissas = [ho.encode(ok, v, want)[0] for v in vals]
+        except ho.Overflow:                      # a denormal next to 1.0 needs more bits than the key has
+            with pytest.raises(FixedPointOverflow):
+                encode_batch(pk, vals)
+            continue
+        got = encode_batch(pk, vals)
+        assert got.exponents == (want,), vals[:4]
+        assert list(got.mantissas) == mantissas
+    big = np.random.default_rng(2).uniform(-1.0, 1.0, size=(3000, 7))
+    eb = encode_batch(pk, big)
+    assert eb.shape == (3000, 7) and eb.exponents == (min(ho.exact_exponent(float(v)) for v in big.ravel()),)
+    assert encode_batch(pk, []).exponents == (0,)
