@@ -74,8 +74,8 @@ class CudaBackend(ExecutionBackend):
         return out
 
     # chunk of the streamed encrypt / obfuscate: a whole number of persistent-grid waves for every limb shape
-    # (lcm of 9472, 7104, 18944, 28416 instances per wave, times two)
-    STREAM_CHUNK = 113664
+    # (lcm of 9472, 7104, 18944, 28416 instances per wave)
+    STREAM_CHUNK = 56832
 
     def encrypt_drawing(self, n: int, src: device.WordArray, rng, obfuscate: bool = False):
         """batch_encrypt / batch_obfuscate with the obfuscation factors drawn while the GPU works: the native
