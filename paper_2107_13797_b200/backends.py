@@ -293,6 +293,20 @@ class CudaBackend(ExecutionBackend):
                 f"|{vals[first]}| needs a mantissa beyond max_int at exponent {exponent} (element {first})")
         return out
 
+    def min_exact_exponent(self, n: int, values) -> int:
+        """min over the values of encoding.exact_exponent (zeros count as 0; 0 for an empty array), on the device."""
+        import numpy as np
+        vals = np.ascontiguousarray(values, dtype=np.float64).ravel()
+        if vals.shape[0] == 0:
+            return 0
+        ctx = device.context_for(n)
+        t = device.torch()
+        dv = t.from_numpy(vals).cuda()
+        lowest = t.full((1,), 2 ** 31 - 1, dtype=t.int32, device="cuda")
+        _native.check(self.lib().hb_min_exact_exponent(ctx.handle, dv.data_ptr(), vals.shape[0], lowest.data_ptr(),
+                                                       self._stream()))
+        return int(lowest.item())
+
     def decode_f64(self, n: int, m: device.WordArray, exponent: int):
         import numpy as np
         from .encoding import FixedPointOverflow

@@ -1,5 +1,6 @@
 // C ABI, second translation unit: hb_powscalar, hb_product, hb_matvec and their device-side helpers
 // (batch modular inversion, bucket-method multi-exponentiation).
+#include <cstdlib>
 #include "hb_ctx.h"
 #include "hb_ops.cuh"
 
@@ -200,11 +201,17 @@ int matvec_ab(hb_ctx* ctx, const uint32_t* c, const PrepOut& pr, long inner, int
   const int cfg = ctx->cfg_pub;
   const int L = Ldig(cfg);
   hb::ModDev mod = dev_mod(ctx->d_pub, ctx->mod_n2);
-  // Window width by row count.  9 bits (1024 buckets per column and window, one window fewer for 52-bit scalars) pays
-  // once the per-window bucket work (about 6 * 2^c multiplications and a 2 * 2^c-step sequential fold) is small next
-  // to the rows; the sorted list packs bucket << 22 | row, so 9 is also the widest that fits with rows < 2^22.
-  int cbits = inner >= 32768 && inner < (1L << 22) ? 9
+  // Window width by row count.  Per column and window the bucket work is about 6 * 2^c multiplications next to one
+  // per row: 9 bits (one window fewer than 8 for 52-bit scalars) pays from 32 k rows, 13 bits (four windows instead
+  // of six) from 400 k rows -- there the fold over the 8192 digit values runs in parallel pieces.
+  int cbits = inner >= 400000 ? 13 : inner >= 32768 ? 9
             : inner >= 4096 ? 8 : inner >= 1024 ? 7 : inner >= 256 ? 6 : inner >= 64 ? 5 : inner >= 16 ? 3 : 2;
+  if (const char* force = getenv("HB_MATVEC_CBITS")) {        // tests: exercise a width whatever the row count
+    const int f = atoi(force);
+    if (f >= 2 && f <= 13) cbits = f;
+  }
+  if (cbits == 13 && (std::max(pr.maxbits, 1) + 12) / 13 >= (std::max(pr.maxbits, 1) + 8) / 9 && !getenv("HB_MATVEC_CBITS"))
+    cbits = 9;                                                 // no window saved: stay with the cheaper buckets
   const int maxbits = std::max(pr.maxbits, 1);
   const int nwin = (maxbits + cbits - 1) / cbits;
   const int NB = 2 << cbits;
@@ -223,7 +230,15 @@ int matvec_ab(hb_ctx* ctx, const uint32_t* c, const PrepOut& pr, long inner, int
   CU(sc.get(&ab, (size_t)d * 2 * L));
   {
     hb::SortArgs A{pr.mag64, pr.neg, inner, d, nwin, cbits, boff, sorted};
-    hb::k_bucket_sort<<<(unsigned)njw, 256, (2 * NB + 1) * sizeof(uint32_t), stream>>>(A);
+    const size_t smem = (2 * (size_t)NB + 1) * sizeof(uint32_t);
+    if (smem > 48 * 1024) {
+      static bool once = false;
+      if (!once) {
+        CU(cudaFuncSetAttribute(hb::k_bucket_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+        once = true;
+      }
+    }
+    hb::k_bucket_sort<<<(unsigned)njw, 256, smem, stream>>>(A);
     g_launches++;
   }
   {
@@ -236,10 +251,35 @@ int matvec_ab(hb_ctx* ctx, const uint32_t* c, const PrepOut& pr, long inner, int
     hb::CombineArgs A{mod, boff, part, d, nwin, cbits, seglen, nseg, bucket};
     HB_DISPATCH(cfg, k_bucket_combine, l, stream, A)
   }
-  {
+  if (cbits <= 9) {
     Launch l = plan(ctx, cfg, (long)njw * 2);
     hb::RunningArgs A{mod, bucket, d, nwin, cbits, win};
     HB_DISPATCH(cfg, k_bucket_running, l, stream, A)
+  } else {
+    const int pieces = 1 << (cbits - 8);                       // 256 digit values per piece
+    uint32_t *tot, *acc;
+    CU(sc.get(&tot, njw * 2 * pieces * L));
+    CU(sc.get(&acc, njw * 2 * pieces * L));
+    hb::RunningSegArgs A{mod, bucket, d, nwin, cbits, pieces, tot, acc};
+    {
+      Launch l = plan(ctx, cfg, (long)njw * 2 * pieces);
+      HB_DISPATCH(cfg, k_bucket_running_seg, l, stream, A)
+    }
+    {
+      Launch l = plan(ctx, cfg, (long)njw * 2);
+      switch (l.cfg) {
+        case 0: hb::k_bucket_running_join<8, 4><<<l.blocks, l.threads, 0, stream>>>(A, win); break;
+        case 1: hb::k_bucket_running_join<16, 4><<<l.blocks, l.threads, 0, stream>>>(A, win); break;
+        case 2: hb::k_bucket_running_join<24, 4><<<l.blocks, l.threads, 0, stream>>>(A, win); break;
+        case 3: hb::k_bucket_running_join<32, 4><<<l.blocks, l.threads, 0, stream>>>(A, win); break;
+        case 4: hb::k_bucket_running_join<24, 8><<<l.blocks, l.threads, 0, stream>>>(A, win); break;
+        case 5: hb::k_bucket_running_join<8, 8><<<l.blocks, l.threads, 0, stream>>>(A, win); break;
+        case 6: hb::k_bucket_running_join<16, 8><<<l.blocks, l.threads, 0, stream>>>(A, win); break;
+        case 7: hb::k_bucket_running_join<8, 16><<<l.blocks, l.threads, 0, stream>>>(A, win); break;
+        default: return fail(HB_ERR_UNSUPPORTED, "no limb configuration");
+      }
+      g_launches++;
+    }
   }
   {
     Launch l = plan(ctx, cfg, (long)d * 2);

@@ -488,7 +488,7 @@ struct SortArgs {
   const uint8_t* neg;      // [d][n]
   long n; int d; int nwin; int cbits;
   uint32_t* boff;          // [d][nwin][NB + 1] exclusive offsets
-  uint32_t* sorted;        // [d][nwin][n]   bucket << 22 | row
+  uint32_t* sorted;        // [d][nwin][n]   rows ordered by bucket (boff delimits the buckets)
 };
 
 __global__ void __launch_bounds__(256) k_bucket_sort(SortArgs A) {
@@ -520,7 +520,7 @@ __global__ void __launch_bounds__(256) k_bucket_sort(SortArgs A) {
     uint32_t v = (uint32_t)(mg[t] >> sh) & vmask;
     uint32_t b = v * 2 + ng[t];
     uint32_t p = atomicAdd(&cur[b], 1u);
-    so[p] = (b << 22) | (uint32_t)t;
+    so[p] = (uint32_t)t;
   }
 }
 
@@ -557,15 +557,26 @@ __global__ void __launch_bounds__(32, 4 * blocks_per_sm(LPT)) k_bucket_segments(
 #pragma unroll
     for (int k = 0; k < LPT; k++) acc[k] = one[k];
     int cur = -1;
+    // bucket of the segment's first entry: the last b with boff[b] <= p0 (empty buckets share an offset)
+    int bk = 2;
+    if (valid && p0 < A.n) {
+      int lo = 2, hi = NB - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if ((long)bo[mid] <= p0) lo = mid; else hi = mid - 1;
+      }
+      bk = lo;
+    }
 #pragma unroll 1
     for (int i = 0; i < A.seglen; i++) {
       long p = p0 + i;
       bool have = valid && p < A.n;
       uint32_t ent = have ? so[p] : 0u;
-      int b = have ? (int)(ent >> 22) : cur;
+      if (have) { while ((long)bo[bk + 1] <= p) bk++; }
+      int b = have ? bk : cur;
       bool change = b != cur;
       if (change && cur >= 0) mt.store_limbs(pt + (seg + cur) * L, acc);
-      if (have) mt.load_limbs(y, A.cm + (long)(ent & 0x3fffffu) * L);
+      if (have) mt.load_limbs(y, A.cm + (long)ent * L);
       else {
 #pragma unroll
         for (int k = 0; k < LPT; k++) y[k] = one[k];
@@ -668,6 +679,88 @@ __global__ void __launch_bounds__(32, 4 * blocks_per_sm(LPT)) k_bucket_running(R
       mt.mul(tot, tot, acc);
     }
     if (valid) mt.store_limbs(A.win + ((j * 2 + s) * A.nwin + w) * L, tot);
+  }
+}
+
+// The same fold in G parallel pieces for wide windows (thousands of buckets make the loop above the longest thing
+// in the call): piece g covers the digit values [lo, hi), lo = 1 + g * len, and produces
+//   tot_g = prod_v B_v^(v - lo + 1)   and   acc_g = prod_v B_v,
+// so that  prod_v B_v^v = prod_g tot_g * acc_g^(lo_g - 1)  (k_bucket_running_join).
+struct RunningSegArgs {
+  ModDev mod;
+  const uint32_t* bucket; int d; int nwin; int cbits; int pieces;
+  uint32_t* tot;           // [d * nwin * 2][pieces][L]
+  uint32_t* acc;           // same shape
+};
+
+template <int LPT, int TPI>
+__global__ void __launch_bounds__(32, 4 * blocks_per_sm(LPT)) k_bucket_running_seg(RunningSegArgs A) {
+  HB_GROUP_PROLOGUE(LPT, TPI)
+  M mt;
+  mt.init(A.mod.n, A.mod.np);
+  const int NB = 2 << A.cbits, NV = 1 << A.cbits;
+  const int len = (NV - 1 + A.pieces - 1) / A.pieces;
+  const long nitems = (long)A.d * A.nwin * 2 * A.pieces;
+  const long ntiles = (nitems + IPW - 1) / IPW;
+  for (long tile = wg; tile < ntiles; tile += nw) {
+    long inst = tile * IPW + g;
+    bool valid = inst < nitems;
+    long it = valid ? inst : nitems - 1;
+    const long jws = it / A.pieces; const int piece = (int)(it - jws * A.pieces);
+    const long jw = jws >> 1; const int s = (int)(jws & 1);
+    const uint32_t* bk = A.bucket + jw * NB * L;
+    const int lo = 1 + piece * len, hi = min(NV, lo + len);
+    uint32_t acc[LPT], tot[LPT], y[LPT];
+    mt.load_limbs(acc, A.mod.r1);
+    mt.load_limbs(tot, A.mod.r1);
+#pragma unroll 1
+    for (int i = 0; i < len; i++) {                  // uniform trip count; values past hi multiply by one
+      const int v = lo + len - 1 - i;
+      if (v < hi) mt.load_limbs(y, bk + (long)(v * 2 + s) * L);
+      else mt.load_limbs(y, A.mod.r1);
+      mt.mul(acc, acc, y);
+      mt.mul(tot, tot, acc);
+    }
+    if (valid) {
+      mt.store_limbs(A.tot + it * L, tot);
+      mt.store_limbs(A.acc + it * L, acc);
+    }
+  }
+}
+
+template <int LPT, int TPI>
+__global__ void __launch_bounds__(32, 4 * blocks_per_sm(LPT)) k_bucket_running_join(RunningSegArgs A, uint32_t* win) {
+  HB_GROUP_PROLOGUE(LPT, TPI)
+  M mt;
+  mt.init(A.mod.n, A.mod.np);
+  const int NV = 1 << A.cbits;
+  const int len = (NV - 1 + A.pieces - 1) / A.pieces;
+  const long nitems = (long)A.d * A.nwin * 2;
+  const long ntiles = (nitems + IPW - 1) / IPW;
+  for (long tile = wg; tile < ntiles; tile += nw) {
+    long inst = tile * IPW + g;
+    bool valid = inst < nitems;
+    long it = valid ? inst : nitems - 1;
+    const long jw = it >> 1; const int s = (int)(it & 1);
+    const long j = jw / A.nwin; const int w = (int)(jw - j * A.nwin);
+    uint32_t total[LPT], x[LPT], y[LPT];
+    mt.load_limbs(total, A.mod.r1);
+#pragma unroll 1
+    for (int piece = 0; piece < A.pieces; piece++) {
+      mt.load_limbs(y, A.tot + (it * A.pieces + piece) * L);
+      mt.mul(total, total, y);
+      // acc^(lo - 1), lo - 1 = piece * len: left-to-right square and multiply, uniform over the warp
+      const int e = piece * len;
+      mt.load_limbs(y, A.acc + (it * A.pieces + piece) * L);
+      mt.load_limbs(x, A.mod.r1);
+#pragma unroll 1
+      for (int b = 30 - __clz(NV | 1) + 1; b >= 0; b--) {
+        mt.mul(x, x, x);
+        if ((e >> b) & 1) mt.mul(x, x, y);
+      }
+      mt.mul(total, total, x);
+    }
+    if (valid) mt.store_limbs(win + ((j * 2 + s) * A.nwin + w) * L, total);
   }
 }
 

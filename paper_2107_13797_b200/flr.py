@@ -98,10 +98,14 @@ def make_minibatches(n_rows: int, batch_size: int, seed: int):
     return [np.asarray(order[i:i + batch_size], dtype=np.intp) for i in range(0, n_rows, batch_size)]
 
 
-def protocol_exponent(values, cap: int = LOGIT_EXPONENT_CAP) -> int:
-    """Exact shared exponent of the values, never coarser than the cap (parties.py:91-96)."""
+def protocol_exponent(values, cap: int = LOGIT_EXPONENT_CAP, pk=None) -> int:
+    """Exact shared exponent of the values, never coarser than the cap (parties.py:91-96).  With a key the minimum
+    is taken on the device (large vectors); the value is the same."""
     values = np.asarray(values, dtype=np.float64)
-    exact = int(encoding.exact_exponents(values).min()) if values.size else 0
+    if pk is not None and values.size >= 4096:
+        exact = default_backend().min_exact_exponent(pk.n, values)
+    else:
+        exact = int(encoding.exact_exponents(values).min()) if values.size else 0
     return min(exact, cap)
 
 
@@ -172,7 +176,7 @@ class HeteroFederation:
         # host -> guest: encrypted logits
         logits_h = self.host_X[idx] @ self.host_theta
         wire = serialize_to_bytes(operators.batch_encrypt(
-            pk, _encode(pk, logits_h, protocol_exponent(logits_h)), self.host_rng, be))
+            pk, _encode(pk, logits_h, protocol_exponent(logits_h, pk=pk)), self.host_rng, be))
         # guest: fore gradient through the arena pipeline, then its gradient slice
         c_lh = deserialize(wire, pk)
         exponent = c_lh.exponents[0]
@@ -212,15 +216,16 @@ class HeteroFederation:
         idx = self.loss_indices
         z_h = self.host_X[idx] @ self.host_theta
         sq = z_h * z_h
-        c1 = operators.batch_encrypt(pk, _encode(pk, z_h, protocol_exponent(z_h)), self.host_rng, be)
-        c2 = operators.batch_encrypt(pk, _encode(pk, sq, protocol_exponent(sq)), self.host_rng, be)
+        c1 = operators.batch_encrypt(pk, _encode(pk, z_h, protocol_exponent(z_h, pk=pk)), self.host_rng, be)
+        c2 = operators.batch_encrypt(pk, _encode(pk, sq, protocol_exponent(sq, pk=pk)), self.host_rng, be)
         c_lh, c_lh2 = deserialize(serialize_to_bytes(c1), pk), deserialize(serialize_to_bytes(c2), pk)
         lg = self.guest_X[idx] @ self.guest_theta
         y = self.guest_y[idx]
         k1 = 0.25 * lg - 0.5 * y
         plain_part = LOG2 - 0.5 * y * lg + 0.125 * lg * lg
         e1, e2 = c_lh.exponents[0], c_lh2.exponents[0]
-        target = min(e1 + protocol_exponent(k1), e2 + encoding.exact_exponent(0.125), protocol_exponent(plain_part))
+        target = min(e1 + protocol_exponent(k1, pk=pk), e2 + encoding.exact_exponent(0.125),
+                     protocol_exponent(plain_part, pk=pk))
         total = operators.batch_add(
             pk,
             operators.batch_mul_plain(pk, c_lh, _encode(pk, k1, target - e1), be),

@@ -610,3 +610,28 @@ def test_default_exponent_found_on_the_device(okeys):
     eb = encode_batch(pk, big)
     assert eb.shape == (3000, 7) and eb.exponents == (min(ho.exact_exponent(float(v)) for v in big.ravel()),)
     assert encode_batch(pk, []).exponents == (0,)
+
+
+@pytest.mark.parametrize("width", ["9", "11", "13"])
+def test_matmul_wide_windows(okeys, monkeypatch, width):
+    """The bucket matvec with the window widths tall matrices use (9 bits from 32 k rows, 13 bits with the
+    piecewise fold from 400 k rows), forced here on small problems: same bits as the oracle."""
+    monkeypatch.setenv("HB_MATVEC_CBITS", width)
+    for name in ("k128", "k1024"):
+        test_matmul(okeys, name)
+    test_matmul_wide(okeys)
+    ok = okeys("k512")
+    pk, sk = product_keys(ok)
+    rng = random.Random(int(width))
+    inner, d = 700, 3
+    pool = ho.k_encrypt(ok, [(rng.randrange(ok.n), ho.draw_unit(ok.n, rng)) for _ in range(6)])
+    cs = [pool[rng.randrange(6)] for _ in range(inner)]
+    ks = []
+    for i in range(inner * d):
+        mag = rng.getrandbits(rng.choice((1, 13, 26, 52, 53, 60)))
+        ks.append(mag if rng.random() < 0.5 else (ok.n - mag) % ok.n)
+    a = CiphertextBatch(pk, (inner,), (-4,), cs, True)
+    x = PlaintextBatch(pk, (inner, d), (-9,), ks, True)
+    got = ops.batch_matmul(pk, a, x)
+    cols = tuple(tuple(ks[t * d + j] for t in range(inner)) for j in range(d))
+    assert list(got.payload) == ho.k_dot(ok, (tuple(cs),), cols, [(0, j) for j in range(d)])
