@@ -203,8 +203,8 @@ int matvec_ab(hb_ctx* ctx, const uint32_t* c, const PrepOut& pr, long inner, int
   hb::ModDev mod = dev_mod(ctx->d_pub, ctx->mod_n2);
   // Window width by row count.  Per column and window the bucket work is about 6 * 2^c multiplications next to one
   // per row: 9 bits (one window fewer than 8 for 52-bit scalars) pays from 32 k rows, 13 bits (four windows instead
-  // of six) from 400 k rows -- there the fold over the 8192 digit values runs in parallel pieces.
-  int cbits = inner >= 400000 ? 13 : inner >= 32768 ? 9
+  // of six) from 200 k rows (measured break-even ~150 k) -- there the fold over the 8192 digit values runs in parallel pieces.
+  int cbits = inner >= 200000 ? 13 : inner >= 32768 ? 9
             : inner >= 4096 ? 8 : inner >= 1024 ? 7 : inner >= 256 ? 6 : inner >= 64 ? 5 : inner >= 16 ? 3 : 2;
   if (const char* force = getenv("HB_MATVEC_CBITS")) {        // tests: exercise a width whatever the row count
     const int f = atoi(force);

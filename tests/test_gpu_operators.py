@@ -615,7 +615,7 @@ def test_default_exponent_found_on_the_device(okeys):
 @pytest.mark.parametrize("width", ["9", "11", "13"])
 def test_matmul_wide_windows(okeys, monkeypatch, width):
     """The bucket matvec with the window widths tall matrices use (9 bits from 32 k rows, 13 bits with the
-    piecewise fold from 400 k rows), forced here on small problems: same bits as the oracle."""
+    piecewise fold from 200 k rows), forced here on small problems: same bits as the oracle."""
     monkeypatch.setenv("HB_MATVEC_CBITS", width)
     for name in ("k128", "k1024"):
         test_matmul(okeys, name)
