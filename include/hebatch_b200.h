@@ -80,8 +80,8 @@ int hb_min_exact_exponent(hb_ctx* ctx, const double* values, int64_t count, int*
 /* Plaintext-side residue arithmetic mod n (batches.py:160-205 of the reference).  plain_mul: out[i] = a[i] * b[i]
  * mod n (b_broadcast != 0 uses b[0]); plain_add: out[i] = a[i] + b[i] mod n; plain_rescale
  * (encoding.py:104-113): the signed mantissa times 16^digits, back as a residue -- first_bad (device int64,
- * preset by the caller to INT64_MAX) receives the smallest index in the overflow band or beyond max_int after
- * scaling. */
+ * preset by the caller to -1, as for the codec) receives the smallest index in the overflow band or beyond max_int
+ * after scaling, or stays -1. */
 int hb_plain_mulmod(hb_ctx* ctx, const uint32_t* a, const uint32_t* b, uint32_t* out, int64_t count,
                     int b_broadcast, void* stream);
 int hb_plain_addmod(hb_ctx* ctx, const uint32_t* a, const uint32_t* b, uint32_t* out, int64_t count, void* stream);
@@ -111,7 +111,8 @@ int hb_product(hb_ctx* ctx, const uint32_t* c, uint32_t* out, int64_t ngroups, i
 int hb_unit_product(hb_ctx* ctx, const uint32_t* r, uint32_t* out, int64_t count, void* stream);
 /* _k_dot / batch_matmul, operators.py:86-94,294-317: c is rows x inner ciphertexts, k is inner x d
  * plaintext residues (row-major), out is rows x d:  out[i][j] = prod_t pow_scalar(c[i][t], k[t][j]).
- * Scalars whose magnitude fits 64 bits take the bucket (Pippenger) path; wider ones a generic path. */
+ * Scalars whose magnitude fits 64 bits take the bucket (Pippenger) path; wider ones a generic path.
+ * inner must be below 2^22 per call. */
 int hb_matvec(hb_ctx* ctx, const uint32_t* c, const uint32_t* k, uint32_t* out, int64_t rows,
               int64_t inner, int64_t d, void* stream);
 
