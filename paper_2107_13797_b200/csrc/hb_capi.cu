@@ -14,8 +14,8 @@ std::atomic<long long> g_launches{0};
 namespace {
 
 // Words of window-table scratch a launch of `count` elements needs (per-warp tiles, see hb_kernels.cuh).
-size_t table_words(const hb_ctx* ctx, int base_cfg, int slots, int64_t count) {
-  Launch l = plan(ctx, base_cfg, count);
+size_t table_words(const hb_ctx* ctx, int base_cfg, int slots, int64_t count, bool encrypt_kernel) {
+  Launch l = plan(ctx, base_cfg, count, encrypt_kernel);
   return (size_t)(slots + 1) * kCfgs[l.cfg].lpt * 32 * l.nwarps;
 }
 
@@ -27,7 +27,7 @@ int encrypt_common(hb_ctx* ctx, const uint32_t* m, const uint32_t* c, const uint
   cudaStream_t stream = (cudaStream_t)stream_;
   CU(cudaSetDevice(ctx->device));
   const int cfg = ctx->cfg_pub;
-  Launch l = plan(ctx, cfg, count);
+  Launch l = plan(ctx, cfg, count, true);
   const long stride = (long)(ctx->slots_n + 1) * kCfgs[l.cfg].lpt * 32;
   uint32_t* tbl = tbl_ext;
   if (!tbl) CU(cudaMallocAsync(&tbl, (size_t)stride * l.nwarps * sizeof(uint32_t), stream));
@@ -40,7 +40,7 @@ int encrypt_common(hb_ctx* ctx, const uint32_t* m, const uint32_t* c, const uint
   A.tbl_stride = stride;
   A.m = m; A.c = c; A.r = r; A.out = out;
   A.count = count; A.wn = ctx->wn; A.wc = ctx->wc; A.mode = mode;
-  HB_DISPATCH_POW(cfg, k_encrypt, l, stream, A)
+  HB_DISPATCH_ENC(cfg, k_encrypt, l, stream, A)
   CU(cudaGetLastError());
   if (!tbl_ext) CU(cudaFreeAsync(tbl, stream));
   return HB_OK;
@@ -352,13 +352,14 @@ static int host_pipeline(hb_ctx* ctx, int kind, const uint32_t* in0, const uint3
   if (cfg < 0) return fail(HB_ERR_NOPRIVATE, "context has no private key");
   const int slots = kind == 0 ? ctx->slots_n : ctx->slots_priv;
   // four full waves of the persistent grid per chunk, so chunking costs no tail
-  const int64_t wave = (int64_t)ctx->sms * 4 * hb::blocks_per_sm(kCfgs[cfg].lpt) * (32 / kCfgs[cfg].tpi);
+  const int tcfg = plan(ctx, cfg, (int64_t)1 << 40, kind == 0).cfg;      // the shape a full chunk runs in
+  const int64_t wave = (int64_t)ctx->sms * 4 * hb::blocks_per_sm(kCfgs[tcfg].lpt) * (32 / kCfgs[tcfg].tpi);
   const int64_t chunk = std::min<int64_t>(count, 4 * wave);
   const int nst = count > chunk ? 2 : 1;
   const int64_t nchunks = (count + chunk - 1) / chunk;
   const int64_t last = count - (nchunks - 1) * chunk;
   const size_t tbl_bytes =
-      sizeof(uint32_t) * std::max(table_words(ctx, cfg, slots, chunk), table_words(ctx, cfg, slots, last));
+      sizeof(uint32_t) * std::max(table_words(ctx, cfg, slots, chunk, kind == 0), table_words(ctx, cfg, slots, last, kind == 0));
   for (int i = 0; i < nst; i++) {
     hb_ctx::HostStage& s = ctx->stage[i];
     if (!s.s) CU(cudaStreamCreateWithFlags(&s.s, cudaStreamNonBlocking));

@@ -1,6 +1,7 @@
 // Shared internals of the C ABI translation units (not part of the public interface).
 #pragma once
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <atomic>
 #include <mutex>
@@ -52,7 +53,8 @@ struct Cfg { int lpt, tpi; };
 // 0..4: one throughput-oriented shape per limb count L = 32, 64, 96, 128, 192 (chosen by modulus size);
 // 5..7: the same L with more lanes per number -- fewer multiplies per thread, so a launch that cannot fill the
 // machine anyway finishes sooner (kernel_cfg picks by element count).  Digit-form arrays only depend on L.
-static const Cfg kCfgs[] = {{8, 4}, {16, 4}, {24, 4}, {32, 4}, {24, 8}, {8, 8}, {16, 8}, {8, 16}};
+// 8: L = 192 on four lanes for the encrypt / obfuscate kernel only (HB_DISPATCH_ENC): b staged in shared memory.
+static const Cfg kCfgs[] = {{8, 4}, {16, 4}, {24, 4}, {32, 4}, {24, 8}, {8, 8}, {16, 8}, {8, 16}, {48, 4}};
 constexpr int kNumCfg = 5;
 
 inline int pick_cfg(int bits) {
@@ -68,7 +70,10 @@ inline int kernel_cfg(int base, long count) {
   }
   return base;
 }
-inline int window_for(int ebits) { return ebits >= 768 ? 5 : ebits >= 160 ? 4 : ebits >= 24 ? 3 : 2; }
+// Sliding-window width by exponent length: multiplications ~ bits / (w + 1) + 2^(w-1) table entries.  Six bits pay
+// from 1024-bit exponents (measured +1.2 % encrypt, +1.3 % decrypt at 2048-bit keys over five); the 33-slot tables
+// (160 MB for the persistent grid at 2048 bits) no longer fit the L2, which the measurement shows not to matter.
+inline int window_for(int ebits) { return ebits >= 1024 ? 6 : ebits >= 768 ? 5 : ebits >= 160 ? 4 : ebits >= 24 ? 3 : 2; }
 
 // Builder of the per-context constant block (one device allocation).
 struct ConstBlock {
@@ -141,8 +146,9 @@ inline hb::ModDev dev_mod(const uint32_t* base, const ModOff& m) {
 
 struct Launch { int blocks; int threads; size_t smem; long nwarps; int cfg; };
 // `base` is the context's shape for the modulus; the launch uses the variant that suits `count` (l.cfg).
-inline Launch plan(const hb_ctx* ctx, int base, long count) {
-  const int cfg = kernel_cfg(base, count);
+inline Launch plan(const hb_ctx* ctx, int base, long count, bool encrypt_kernel = false) {
+  int cfg = kernel_cfg(base, count);
+  if (encrypt_kernel && cfg == 4 && count > 14208) cfg = 8;      // L = 192 at throughput counts: (48, 4)
   const int tpi = kCfgs[cfg].tpi, lpt = kCfgs[cfg].lpt;
   const int ipw = 32 / tpi;
   long ntiles = (count + ipw - 1) / ipw;
@@ -202,6 +208,16 @@ constexpr size_t sqr_smem_bytes() { return (size_t)hb::Mont<LPT, TPI>::SQ_WORDS 
 #else
 #define HB_DISPATCH_POW HB_DISPATCH
 #endif
+
+// k_encrypt: the nine shapes; (48, 4) takes its staging area as dynamic shared memory.
+#define HB_DISPATCH_ENC(cfg, KERNEL, launch, stream, args)                                              \
+  if (launch.cfg == 8) {                                                                                \
+    hb::KERNEL<48, 4><<<launch.blocks, launch.threads,                                                  \
+                        hb::Mont<48, 4>::STAGE_WORDS * hb::Mont<48, 4>::IPW * sizeof(uint32_t), stream>>>(args); \
+    hbi::g_launches++;                                                                                  \
+  } else {                                                                                              \
+    HB_DISPATCH_POW(cfg, KERNEL, launch, stream, args)                                                  \
+  }
 
 #define HB_DISPATCH(cfg, KERNEL, launch, stream, args)                                           \
   switch (launch.cfg) {                                                                                 \

@@ -35,6 +35,16 @@ __device__ __forceinline__ void run_prog(const Mont<LPT, TPI>& mt, uint32_t (&x)
     if (kind == OP_LOAD) {
       tile_load<LPT>(tw, src, x);
     } else if (kind != OP_KEEP) {
+      if constexpr (LPT == 48) {              // wide-lane shape: b comes from shared memory (Mont::mul_sf)
+        uint32_t y[LPT];
+        if (kind == OP_MUL) {
+          tile_load<LPT>(tw, src, y);
+        } else {
+#pragma unroll
+          for (int k = 0; k < LPT; k++) y[k] = x[k];
+        }
+        mt.mul_sf(x, x, y, sw);
+      } else
 #ifdef HB_USE_SQR
       if constexpr (Mont<LPT, TPI>::HAS_SQR) {
         if (kind == OP_MUL) {
@@ -66,7 +76,9 @@ extern __shared__ uint32_t hb_dyn_smem[];
 template <int LPT, int TPI>
 __device__ __forceinline__ uint32_t* sqr_scratch() {
   using M = Mont<LPT, TPI>;
-  if constexpr (M::HAS_SQR) {
+  if constexpr (LPT == 48) {
+    return hb_dyn_smem + threadIdx.x / TPI;        // staging area only (Mont::mul_sf), one warp per block
+  } else if constexpr (M::HAS_SQR) {
     return hb_dyn_smem + threadIdx.x / TPI;        // one warp per block
   } else {
     return nullptr;

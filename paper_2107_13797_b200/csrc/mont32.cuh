@@ -365,6 +365,44 @@ struct Mont {
     finish(r, E, O, pend_lo, pend_hi);
   }
 
+  // mul() with b read from shared memory and the rows of one lane block fully unrolled (no frame-rotation moves):
+  // the form for LPT = 48, where a register copy of b would not fit next to the accumulators, a and n.
+  // `sa`: this instance's staging area alone, STAGE_WORDS words at stride IPW.
+  static constexpr int STAGE_WORDS = L + TPI;
+  __device__ __forceinline__ void mul_sf(uint32_t (&r)[LPT], const uint32_t (&a)[LPT], const uint32_t (&b)[LPT],
+                                         uint32_t* sa) const {
+    uint64_t E[H + 1], O[H + 1];
+#pragma unroll
+    for (int i = 0; i <= H; i++) { E[i] = 0; O[i] = 0; }
+    uint32_t pend_lo = 0, pend_hi = 0;
+    __syncwarp();
+    {
+      uint32_t* d = sa + ((LPT + 1) * t) * IPW;
+#pragma unroll
+      for (int k = 0; k < LPT; k++) d[k * IPW] = b[k];
+    }
+    __syncwarp();
+#pragma unroll 1
+    for (int s = 0; s < TPI; s++) {
+      const uint32_t* bs = sa + ((LPT + 1) * s) * IPW;
+#pragma unroll
+      for (int i = 0; i < LPT; i++) {
+        mac_row(E, O, a, bs[i * IPW]);
+        uint32_t q = (lo32(E[0]) + pend_lo) * np;
+        q = __shfl_sync(FULLMASK, q, 0, TPI);
+        mac_row(E, O, n, q);
+        const uint32_t vlo = add_cc32(lo32(E[0]), pend_lo);
+        const uint32_t vhi = addc_cc32(hi32(E[0]), pend_hi);
+        const uint32_t vtop = addc32(0, 0);
+        const uint32_t recv = __shfl_sync(FULLMASK, vlo, t + 1, TPI);    // top lane wraps to lane 0: zero
+        pend_lo = vhi;
+        pend_hi = vtop;
+        frame_down(E, O, recv);
+      }
+    }
+    finish(r, E, O, pend_lo, pend_hi);
+  }
+
   // r = a * a / R mod n, canonical.  sw: this instance's shared-memory scratch (SQ_WORDS words, stride IPW).
   __device__ __forceinline__ void sqr(uint32_t (&r)[LPT], const uint32_t (&a)[LPT], uint32_t* sw) const {
     constexpr int W = 2 * LPT;

@@ -51,7 +51,7 @@ def test_squaring_all_ones_modulus():
         assert list(got) == [pow(v, 8, n2) for v in vals]
 
 
-@pytest.mark.parametrize("key_bits,count", [(1024, 20000), (2048, 19200)])
+@pytest.mark.parametrize("key_bits,count", [(1024, 20000), (2048, 19200), (3072, 15000)])
 def test_large_batch_shapes_round_trip(key_bits, count):
     """Encrypt / decrypt at counts that select the throughput shapes ((16,4)/(32,4) at 2048 bits), checked by
     the size-independent round trip and, on a prefix, bit for bit against Python integers."""
