@@ -635,3 +635,55 @@ def test_matmul_wide_windows(okeys, monkeypatch, width):
     got = ops.batch_matmul(pk, a, x)
     cols = tuple(tuple(ks[t * d + j] for t in range(inner)) for j in range(d))
     assert list(got.payload) == ho.k_dot(ok, (tuple(cs),), cols, [(0, j) for j in range(d)])
+
+
+def test_large_batch_properties():
+    """Size-independent properties at a batch size in the range of BASELINE's configs (200 k elements, Paillier-2048,
+    where every kernel runs in its throughput shape): decrypt(encrypt) round trip, additivity of hadd, scalar
+    multiplication by positive and negative constants, the sum reduction against its two halves and against the
+    plaintext sum, and the encrypted matvec against integer arithmetic."""
+    import numpy as np
+    from paper_2107_13797_b200.device import WordArray
+    keys = paillier.keygen(2048, paillier.default_rng(7), allow_insecure=True)
+    pk, sk = keys.public, keys.private
+    n = pk.n
+    count, wn = 200_000, 64
+    rs = np.random.default_rng(11)
+    m = np.zeros((count, wn), dtype=np.uint32)
+    m[:, 0] = rs.integers(0, 1 << 32, size=count, dtype=np.uint64).astype(np.uint32)
+    m[:, 1] = rs.integers(0, 1 << 20, size=count, dtype=np.uint64).astype(np.uint32)          # 52-bit values
+    vals = m[:, 0].astype(object) + (m[:, 1].astype(object) << 32)
+    plain = PlaintextBatch(pk, (count,), (-8,), WordArray.from_numpy(m), True)
+    c = ops.batch_encrypt(pk, plain, random.Random(1))
+    assert np.array_equal(ops.batch_decrypt(sk, c).words.numpy(), m)
+    # hadd: Dec(c_i * c_(count-1-i)) = m_i + m_(count-1-i)
+    rev = CiphertextBatch(pk, (count,), (-8,), WordArray.from_numpy(c.words.numpy()[::-1].copy()), True, True)
+    both = ops.batch_decrypt(sk, ops.batch_add(pk, c, rev)).words.numpy()
+    want = vals + vals[::-1]
+    got = both[:, 0].astype(object) + (both[:, 1].astype(object) << 32)
+    assert (got == want).all() and not both[:, 2:].any()
+    # hmul by 3 and by -2 (the inverse-base branch)
+    three = PlaintextBatch(pk, (1,), (0,), (3,), True)
+    t3 = ops.batch_decrypt(sk, ops.batch_mul_plain(pk, c, three)).words.numpy()
+    assert ((t3[:, 0].astype(object) + (t3[:, 1].astype(object) << 32)) == 3 * vals).all()
+    minus2 = PlaintextBatch(pk, (1,), (0,), (n - 2,), True)
+    neg = ops.batch_decrypt(sk, ops.batch_mul_plain(pk, c, minus2))
+    sample = [0, 1, 777, count // 2, count - 1]
+    assert [neg.mantissas[i] for i in sample] == [(n - 2 * int(vals[i])) % n for i in sample]
+    # hsum: whole == product of the halves, decrypts to the plaintext sum
+    total = ops.batch_sum(pk, c)
+    half = count // 2
+    lo = CiphertextBatch(pk, (half,), (-8,), WordArray.from_numpy(c.words.numpy()[:half]), True, True)
+    hi = CiphertextBatch(pk, (count - half,), (-8,), WordArray.from_numpy(c.words.numpy()[half:]), True, True)
+    assert ops.batch_add(pk, ops.batch_sum(pk, lo), ops.batch_sum(pk, hi)).payload == total.payload
+    assert ops.batch_decrypt(sk, total).mantissas[0] == int(vals.sum()) % n
+    # matvec (13-bit windows at this height): 200 k x 3 signed 40-bit scalars
+    d = 3
+    mag = rs.integers(0, 1 << 40, size=(count, d), dtype=np.int64)
+    sgn = rs.integers(0, 2, size=(count, d), dtype=np.int64) * 2 - 1
+    x = (mag * sgn).astype(np.float64)
+    xb = encode_batch(pk, x, target_exponent=0)
+    out = ops.batch_decrypt(sk, ops.batch_matmul(pk, c, xb))
+    signed = (mag * sgn).astype(object)
+    for j in range(d):
+        assert out.mantissas[j] == int((vals * signed[:, j]).sum()) % n
