@@ -20,6 +20,15 @@ HB_ERR_UNSUPPORTED = -3
 HB_ERR_NOPRIVATE = -4
 HB_ERR_NOTUNIT = -5
 
+# flags of the *_rep entry points / hb_powscalar (include/hebatch_b200.h)
+HB_POW_RAW_EXPONENT = 1
+HB_A_MONT = 0x10
+HB_B_MONT = 0x20
+HB_OUT_MONT = 0x40
+HB_OPT_MATVEC_WINDOW_BITS = 1
+HB_OPT_POOL_KEEP_BYTES = 2
+HB_OPT_MATVEC_BLOCK_ROWS = 3
+
 
 class NativeLibraryError(RuntimeError):
     """The CUDA library is missing, was not built, or a call into it failed."""
@@ -39,6 +48,22 @@ SIGNATURES = {
     "hb_ctx_create": (_int, [ctypes.POINTER(_vp), _vp, _int, _int]),
     "hb_ctx_set_private": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _int]),
     "hb_ctx_destroy": (None, [_vp]),
+    "hb_ctx_set_option": (_int, [_vp, _int, _i64]),
+    "hb_ct_limbs": (_int, [_vp]),
+    "hb_ct_convert": (_int, [_vp, _vp, _vp, _i64, _int, _vp]),
+    "hb_encrypt_rep": (_int, [_vp, _vp, _vp, _vp, _i64, _int, _vp]),
+    "hb_obfuscate_rep": (_int, [_vp, _vp, _vp, _vp, _i64, _int, _vp]),
+    "hb_decrypt_rep": (_int, [_vp, _vp, _vp, _i64, _int, _vp]),
+    "hb_mulmod_rep": (_int, [_vp, _vp, _vp, _vp, _i64, _int, _int, _vp]),
+    "hb_lift_mulmod_rep": (_int, [_vp, _vp, _vp, _vp, _i64, _int, _int, _vp]),
+    "hb_fore_gradient": (_int, [_vp, _vp, _vp, _vp, ctypes.c_uint32, _vp, _vp, _vp, _i64, _int, _vp]),
+    "hb_product_rep": (_int, [_vp, _vp, _vp, _i64, _i64, _i64, _i64, _int, _vp]),
+    "hb_matvec_rep": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _int, _vp]),
+    "hb_scalar_compact": (_int, [_vp, _vp, _i64, _i64, _vp, _vp, _vp, _vp]),
+    "hb_encode_f64_compact": (_int, [_vp, _vp, _int, _i64, _i64, _vp, _vp, _vp, _vp]),
+    "hb_matvec_compact": (_int, [_vp, _vp, _vp, _vp, _int, _int, _vp, _i64, _i64, _int, _vp]),
+    "hb_matvec_partial_compact": (_int, [_vp, _vp, _vp, _vp, _int, _vp, _i64, _i64, _int, _vp]),
+    "hb_secure_randrange1": (_int, [_vp, _int, _i64, _vp]),
     "hb_pt_words": (_int, [_vp]),
     "hb_ct_words": (_int, [_vp]),
     "hb_key_bits": (_int, [_vp]),

@@ -61,6 +61,8 @@ class _Batch:
             store = values                     # produced by an operator: in range by construction
             if store.count != count:
                 raise ShapeMismatch(f"payload length {store.count} does not match shape {shape}")
+            if store.width != width:
+                raise ValueError(f"word storage is {store.width} words per {self._what}, this key needs {width}")
         else:
             values = tuple(values)
             if len(values) != count:
@@ -174,23 +176,37 @@ def _flatten(values):
     return np.asarray([float(v) for v in values], dtype=np.float64), (len(values),)
 
 
-def encode_batch(pk: PublicKey, values, shape=None, target_exponent: int | None = None) -> PlaintextBatch:
+def encode_batch(pk: PublicKey, values, shape=None, target_exponent: int | None = None, backend=None,
+                 compact: bool = False) -> PlaintextBatch:
     """Encode a flat or nested sequence (or a numpy array) under one shared exponent (batches.py:112-125): the
-    minimum of the exact exponents unless a target is given.  The mantissas are produced by the GPU codec."""
-    from . import operators
+    minimum of the exact exponents unless a target is given.  The mantissas are produced by the GPU codec.
+
+    compact=True (2-D input, the right operand of batch_matmul): keep the matrix in the compact resident form --
+    sign + 64-bit magnitude per scalar, 9 bytes instead of a full residue -- which is all the encrypted matvec reads;
+    `mantissas` are still there, materialised on demand.  The role of MiniBatchAggregator (bufferpool.py:182-226)."""
+    from .backends import default_backend
     flat, inferred = _flatten(values)
     if shape is None:
         shape = inferred
+    shape = tuple(shape)
     if target_exponent is None and flat.size == 0:
         target_exponent = 0
-    plain = operators.batch_encode(pk, flat, target_exponent)      # None: the exact shared exponent, found on the device
-    return PlaintextBatch(pk, tuple(shape), plain.exponents, plain.words, True)
+    if flat.size == 0:
+        return PlaintextBatch(pk, shape, (target_exponent or 0,), (), True)
+    be = backend or default_backend()
+    if compact and len(shape) == 2:
+        packed = be.encode_compact(pk.n, flat.reshape(shape), target_exponent)
+        if packed is not None:
+            return PlaintextBatch(pk, shape, (packed[1],), packed[0], True)
+    # None: the exact shared exponent, found on the device
+    words, used = be.encode_f64(pk.n, flat, target_exponent, row_width=shape[1] if len(shape) == 2 else 1)
+    return PlaintextBatch(pk, shape, (used,), words, True)
 
 
-def decode_batch(pk: PublicKey, batch: PlaintextBatch) -> list:
+def decode_batch(pk: PublicKey, batch: PlaintextBatch, backend=None) -> list:
     from . import operators
     if batch.shared_exponent or len(set(batch.exponents)) <= 1:
-        return operators.batch_decode(pk, batch)
+        return operators.batch_decode(pk, batch, backend)
     return [encoding.decode(pk, batch.element(i)) for i in range(batch.count)]
 
 
@@ -208,9 +224,10 @@ def shared_exponent_of(batch) -> int:
     return first
 
 
-def plain_rescale(batch: PlaintextBatch, new_exponent: int) -> PlaintextBatch:
+def plain_rescale(batch: PlaintextBatch, new_exponent: int, backend=None) -> PlaintextBatch:
     """Exact re-grid of every element onto a finer shared exponent (batches.py:160-170), on the device."""
     from .backends import default_backend
+    be = backend or default_backend()
     current = shared_exponent_of(batch)
     if new_exponent == current:
         return batch
@@ -219,7 +236,7 @@ def plain_rescale(batch: PlaintextBatch, new_exponent: int) -> PlaintextBatch:
         raise ValueError("can only rescale toward a smaller exponent")
     if batch.count == 0:
         return PlaintextBatch(pk, batch.shape, (new_exponent,), (), True)
-    words, bad = default_backend().plain_rescale(pk.n, batch.words, current - new_exponent)
+    words, bad = be.plain_rescale(pk.n, batch.words, current - new_exponent)
     if bad >= 0:
         # the reference fails on the first offending element; let the scalar codec name the error
         encoding.rescale(pk, batch.element(bad), new_exponent)
@@ -227,21 +244,22 @@ def plain_rescale(batch: PlaintextBatch, new_exponent: int) -> PlaintextBatch:
     return PlaintextBatch(pk, batch.shape, (new_exponent,), words, True)
 
 
-def plain_mul(a: PlaintextBatch, b: PlaintextBatch) -> PlaintextBatch:
+def plain_mul(a: PlaintextBatch, b: PlaintextBatch, backend=None) -> PlaintextBatch:
     """Encoded product, element-wise or by one broadcast scalar: mantissas multiply mod n, exponents
     add (batches.py:173-192).  The residues are multiplied on the device."""
     from .backends import default_backend
+    dev = backend or default_backend()
     require_same_key(a, b)
     pk = a.key
     if b.count == 1:
         be = b.exponent_at(0)
-        prod = default_backend().plain_mulmod(pk.n, a.words, b.words, True) if a.count else a.words
+        prod = dev.plain_mulmod(pk.n, a.words, b.words, True) if a.count else a.words
         if a.shared_exponent:
             return PlaintextBatch(pk, a.shape, (a.exponents[0] + be,), prod, True)
         return PlaintextBatch(pk, a.shape, tuple(e + be for e in a.exponents), prod, False)
     if a.shape != b.shape:
         raise ShapeMismatch(f"{a.shape} vs {b.shape}")
-    prod = default_backend().plain_mulmod(pk.n, a.words, b.words) if a.count else a.words
+    prod = dev.plain_mulmod(pk.n, a.words, b.words) if a.count else a.words
     if a.shared_exponent and b.shared_exponent:
         return PlaintextBatch(pk, a.shape, (a.exponents[0] + b.exponents[0],), prod, True)
     exps = tuple(a.exponent_at(i) + b.exponent_at(i) for i in range(a.count))
@@ -249,13 +267,14 @@ def plain_mul(a: PlaintextBatch, b: PlaintextBatch) -> PlaintextBatch:
     return PlaintextBatch(pk, a.shape, exps[:1] if shared else exps, prod, shared)
 
 
-def plain_add(a: PlaintextBatch, b: PlaintextBatch) -> PlaintextBatch:
+def plain_add(a: PlaintextBatch, b: PlaintextBatch, backend=None) -> PlaintextBatch:
     """Encoded sum after exact alignment to the finer exponent (batches.py:195-205), on the device."""
     from .backends import default_backend
+    dev = backend or default_backend()
     require_same_key(a, b)
     if a.shape != b.shape:
         raise ShapeMismatch(f"{a.shape} vs {b.shape}")
     target = min(shared_exponent_of(a), shared_exponent_of(b))
-    a, b = plain_rescale(a, target), plain_rescale(b, target)
-    total = default_backend().plain_addmod(a.key.n, a.words, b.words) if a.count else a.words
+    a, b = plain_rescale(a, target, dev), plain_rescale(b, target, dev)
+    total = dev.plain_addmod(a.key.n, a.words, b.words) if a.count else a.words
     return PlaintextBatch(a.key, a.shape, (target,), total, True)

@@ -9,6 +9,36 @@ using namespace hbi;
 namespace hbi {
 thread_local std::string g_err;
 std::atomic<long long> g_launches{0};
+
+namespace {
+std::mutex g_pool_mu;
+cudaMemPool_t g_pools[64] = {};
+}
+// Window tables (160 MB for a full encrypt grid at 2048 bits) and the matvec scratch (GBs at 1 M rows) are taken
+// per call.  Blocks freed by a call stay in the pool up to this many bytes across synchronisations, so that a loop
+// of small calls allocates nothing; what lies beyond goes back to the driver, leaving the memory to the
+// application's own allocator (torch's caching allocator holds the batches themselves).
+constexpr unsigned long long kPoolKeepDefault = 1ull << 30;
+
+cudaMemPool_t device_pool(int device) {
+  if (device < 0 || device >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(g_pool_mu);
+  if (g_pools[device]) return g_pools[device];
+  cudaMemPoolProps props{};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.handleTypes = cudaMemHandleTypeNone;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = device;
+  cudaMemPool_t pool = nullptr;
+  if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+  unsigned long long keep = kPoolKeepDefault;
+  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  g_pools[device] = pool;
+  return pool;
+}
+cudaError_t pool_alloc(cudaMemPool_t pool, void** p, size_t bytes, cudaStream_t stream) {
+  return cudaMallocFromPoolAsync(p, bytes ? bytes : 1, pool, stream);
+}
 }
 
 namespace {
@@ -20,7 +50,7 @@ size_t table_words(const hb_ctx* ctx, int base_cfg, int slots, int64_t count, bo
 }
 
 int encrypt_common(hb_ctx* ctx, const uint32_t* m, const uint32_t* c, const uint32_t* r, uint32_t* out,
-                   int64_t count, int mode, void* stream_, uint32_t* tbl_ext = nullptr) {
+                   int64_t count, int mode, void* stream_, uint32_t* tbl_ext = nullptr, int flags = 0) {
   if (!ctx || !r || !out || (mode == 0 ? !m : !c)) return fail(HB_ERR_ARG, "null pointer");
   if (count < 0) return fail(HB_ERR_ARG, "negative count");
   if (count == 0) return HB_OK;
@@ -30,10 +60,12 @@ int encrypt_common(hb_ctx* ctx, const uint32_t* m, const uint32_t* c, const uint
   Launch l = plan(ctx, cfg, count, true);
   const long stride = (long)(ctx->slots_n + 1) * kCfgs[l.cfg].lpt * 32;
   uint32_t* tbl = tbl_ext;
-  if (!tbl) CU(cudaMallocAsync(&tbl, (size_t)stride * l.nwarps * sizeof(uint32_t), stream));
+  if (!tbl) CU(pool_alloc(ctx->pool, (void**)&tbl, (size_t)stride * l.nwarps * sizeof(uint32_t), stream));
   hb::EncArgs A;
   A.mod = dev_mod(ctx->d_pub, ctx->mod_n2);
-  A.nR = ctx->d_pub + ctx->off_nR;
+  A.c_mont = (flags & HB_A_MONT) ? 1 : 0;
+  A.out_mont = (flags & HB_OUT_MONT) ? 1 : 0;
+  A.nR = ctx->d_pub + (A.out_mont ? ctx->off_nR2 : ctx->off_nR);
   A.prog = ctx->d_pub + ctx->off_prog_n;
   A.nprog = ctx->nprog_n;
   A.tbl = tbl;
@@ -47,7 +79,7 @@ int encrypt_common(hb_ctx* ctx, const uint32_t* m, const uint32_t* c, const uint
 }
 
 int mulmod_common(hb_ctx* ctx, const uint32_t* a, const uint32_t* b, uint32_t* out, int64_t count,
-                  int lift, int bcast, void* stream_) {
+                  int lift, int bcast, void* stream_, int flags = 0) {
   if (!ctx || !a || !b || !out) return fail(HB_ERR_ARG, "null pointer");
   if (count < 0) return fail(HB_ERR_ARG, "negative count");
   if (count == 0) return HB_OK;
@@ -58,8 +90,13 @@ int mulmod_common(hb_ctx* ctx, const uint32_t* a, const uint32_t* b, uint32_t* o
   hb::MulArgs A;
   A.mod = dev_mod(ctx->d_pub, ctx->mod_n2);
   A.nR = ctx->d_pub + ctx->off_nR;
+  A.nR2 = ctx->d_pub + ctx->off_nR2;
+  A.r3 = ctx->d_pub + ctx->off_R3;
   A.a = a; A.b = b; A.out = out; A.count = count; A.wn = ctx->wn; A.wc = ctx->wc;
   A.lift = lift; A.b_broadcast = bcast;
+  A.a_mont = (flags & HB_A_MONT) ? 1 : 0;
+  A.b_mont = (!lift && (flags & HB_B_MONT)) ? 1 : 0;
+  A.out_mont = (flags & HB_OUT_MONT) ? 1 : 0;
   HB_DISPATCH(cfg, k_mulmod, l, stream, A)
   CU(cudaGetLastError());
   return HB_OK;
@@ -81,18 +118,11 @@ int hb_ctx_create(hb_ctx** out, const uint32_t* n_words, int n_nwords, int devic
   CU(cudaGetDeviceCount(&ndev));
   if (device < 0 || device >= ndev) return fail(HB_ERR_CUDA, "no such CUDA device");
   CU(cudaSetDevice(device));
-  {
-    // every operator takes its scratch from the stream-ordered allocator; keep freed blocks in the pool instead of
-    // handing them back to the driver at each synchronisation (the default release threshold is zero)
-    cudaMemPool_t pool = nullptr;
-    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess && pool) {
-      unsigned long long keep = ~0ull;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    }
-    cudaGetLastError();
-  }
+  cudaMemPool_t pool = device_pool(device);
+  if (!pool) return fail(HB_ERR_CUDA, "cannot create the library's memory pool on this device");
   hb_ctx* ctx = new hb_ctx();
   ctx->device = device;
+  ctx->pool = pool;
   cudaDeviceProp prop;
   cudaError_t e = cudaGetDeviceProperties(&prop, device);
   if (e != cudaSuccess) { delete ctx; return fail(HB_ERR_CUDA, cudaGetErrorString(e)); }
@@ -108,6 +138,11 @@ int hb_ctx_create(hb_ctx** out, const uint32_t* n_words, int n_nwords, int devic
   ConstBlock cb;
   ctx->mod_n2 = add_modulus(cb, ctx->n2, L);
   ctx->off_nR = cb.add(hbh::to_limbs(hbh::shl_mod(n, 32L * L, ctx->n2), L));
+  ctx->off_nR2 = cb.add(hbh::to_limbs(hbh::shl_mod(n, 2 * 32L * L, ctx->n2), L));
+  {
+    Big one{1};
+    ctx->off_R3 = cb.add(hbh::to_limbs(hbh::shl_mod(one, 3 * 32L * L, ctx->n2), L));
+  }
   ctx->cfg_n = pick_cfg(ctx->key_bits);
   ctx->mod_n_pub = add_modulus(cb, n, kCfgs[ctx->cfg_n].lpt * kCfgs[ctx->cfg_n].tpi);
   std::vector<uint32_t> prog = hbh::build_program(n, window_for(ctx->key_bits), &ctx->slots_n);
@@ -185,8 +220,9 @@ int hb_ctx_set_private(hb_ctx* ctx, const uint32_t* p_, const uint32_t* q_, cons
   ctx->mod_n_priv = add_modulus(cb, ctx->n, L);
   ctx->off_qR = cb.add(hbh::to_limbs(hbh::shl_mod(q, 32L * L, ctx->n), L));
   ctx->slots_priv = slots;
-  if (ctx->d_priv) { cudaFree(ctx->d_priv); ctx->d_priv = nullptr; }
-  CU(cudaMalloc(&ctx->d_priv, cb.host.size() * sizeof(uint32_t)));
+  if (ctx->d_priv) { cudaMemset(ctx->d_priv, 0, ctx->priv_bytes); cudaFree(ctx->d_priv); ctx->d_priv = nullptr; }
+  ctx->priv_bytes = cb.host.size() * sizeof(uint32_t);
+  CU(cudaMalloc(&ctx->d_priv, ctx->priv_bytes));
   CU(cudaMemcpy(ctx->d_priv, cb.host.data(), cb.host.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
   ctx->cfg_priv = cfg;
   ctx->has_private = true;
@@ -200,9 +236,34 @@ void hb_ctx_destroy(hb_ctx* ctx) {
   cudaSetDevice(ctx->device);
   release_stages(ctx);
   if (ctx->d_pub) cudaFree(ctx->d_pub);
-  if (ctx->d_priv) cudaFree(ctx->d_priv);
-  if (ctx->codec_scratch) cudaFree(ctx->codec_scratch);
+  if (ctx->d_priv) {                  // private constants do not outlive the context in HBM
+    cudaMemset(ctx->d_priv, 0, ctx->priv_bytes);
+    cudaFree(ctx->d_priv);
+  }
   delete ctx;
+}
+
+int hb_ctx_set_option(hb_ctx* ctx, int option, int64_t value) {
+  if (!ctx) return fail(HB_ERR_ARG, "null pointer");
+  switch (option) {
+    case HB_OPT_MATVEC_WINDOW_BITS:
+      if (value != 0 && (value < 2 || value > 13)) return fail(HB_ERR_ARG, "matvec window must be 0 (auto) or 2..13 bits");
+      ctx->opt_matvec_cbits = (int)value;
+      return HB_OK;
+    case HB_OPT_MATVEC_BLOCK_ROWS:
+      if (value < 0) return fail(HB_ERR_ARG, "negative block size");
+      ctx->opt_matvec_block = (long)value;
+      return HB_OK;
+    case HB_OPT_POOL_KEEP_BYTES: {
+      if (value < 0) return fail(HB_ERR_ARG, "negative pool threshold");
+      CU(cudaSetDevice(ctx->device));
+      unsigned long long keep = (unsigned long long)value;
+      CU(cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrReleaseThreshold, &keep));
+      return HB_OK;
+    }
+    default:
+      return fail(HB_ERR_ARG, "unknown option");
+  }
 }
 
 int hb_pt_words(const hb_ctx* ctx) { return ctx ? ctx->wn : 0; }
@@ -215,6 +276,14 @@ int hb_encrypt(hb_ctx* ctx, const uint32_t* m, const uint32_t* r, uint32_t* out,
 int hb_obfuscate(hb_ctx* ctx, const uint32_t* c, const uint32_t* r, uint32_t* out, int64_t count, void* stream) {
   return encrypt_common(ctx, nullptr, c, r, out, count, 1, stream);
 }
+int hb_encrypt_rep(hb_ctx* ctx, const uint32_t* m, const uint32_t* r, uint32_t* out, int64_t count, int flags,
+                   void* stream) {
+  return encrypt_common(ctx, m, nullptr, r, out, count, 0, stream, nullptr, flags & HB_OUT_MONT);
+}
+int hb_obfuscate_rep(hb_ctx* ctx, const uint32_t* c, const uint32_t* r, uint32_t* out, int64_t count, int flags,
+                     void* stream) {
+  return encrypt_common(ctx, nullptr, c, r, out, count, 1, stream, nullptr, flags & (HB_A_MONT | HB_OUT_MONT));
+}
 int hb_mulmod(hb_ctx* ctx, const uint32_t* a, const uint32_t* b, uint32_t* out, int64_t count,
               int b_broadcast, void* stream) {
   return mulmod_common(ctx, a, b, out, count, 0, b_broadcast, stream);
@@ -222,6 +291,45 @@ int hb_mulmod(hb_ctx* ctx, const uint32_t* a, const uint32_t* b, uint32_t* out, 
 int hb_lift_mulmod(hb_ctx* ctx, const uint32_t* a, const uint32_t* m, uint32_t* out, int64_t count,
                    int m_broadcast, void* stream) {
   return mulmod_common(ctx, a, m, out, count, 1, m_broadcast, stream);
+}
+int hb_mulmod_rep(hb_ctx* ctx, const uint32_t* a, const uint32_t* b, uint32_t* out, int64_t count,
+                  int b_broadcast, int flags, void* stream) {
+  return mulmod_common(ctx, a, b, out, count, 0, b_broadcast, stream, flags);
+}
+int hb_lift_mulmod_rep(hb_ctx* ctx, const uint32_t* a, const uint32_t* m, uint32_t* out, int64_t count,
+                       int m_broadcast, int flags, void* stream) {
+  return mulmod_common(ctx, a, m, out, count, 1, m_broadcast, stream, flags);
+}
+
+int hb_fore_gradient(hb_ctx* ctx, const uint32_t* c, const uint32_t* lg, const uint32_t* kg, uint32_t kh,
+                     const uint32_t* yl, const uint32_t* r, uint32_t* out, int64_t count, int flags,
+                     void* stream_) {
+  if (!ctx || !c || !lg || !kg || !yl || !r || !out) return fail(HB_ERR_ARG, "null pointer");
+  if (count < 0) return fail(HB_ERR_ARG, "negative count");
+  if (kh < 1) return fail(HB_ERR_ARG, "the ciphertext exponent must be at least 1");
+  if (count == 0) return HB_OK;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  CU(cudaSetDevice(ctx->device));
+  const int cfg = ctx->cfg_pub;
+  Launch l = plan(ctx, cfg, count, true);
+  const int spare = ctx->slots_n;                       // table slots [0, slots_n) belong to the exponent program
+  const long stride = (long)(spare + 2) * kCfgs[l.cfg].lpt * 32;
+  uint32_t* tbl = nullptr;
+  CU(pool_alloc(ctx->pool, (void**)&tbl, (size_t)stride * l.nwarps * sizeof(uint32_t), stream));
+  hb::ForeArgs A;
+  A.mod = dev_mod(ctx->d_pub, ctx->mod_n2);
+  A.nR2 = ctx->d_pub + ctx->off_nR2;
+  A.prog = ctx->d_pub + ctx->off_prog_n;
+  A.nprog = ctx->nprog_n;
+  A.tbl = tbl; A.tbl_stride = stride; A.spare = spare;
+  A.lg = lg; A.kg = kg; A.c = c; A.yl = yl; A.r = r; A.out = out; A.kh = kh;
+  A.count = count; A.wn = ctx->wn; A.wc = ctx->wc;
+  A.c_mont = (flags & HB_A_MONT) ? 1 : 0;
+  A.out_mont = (flags & HB_OUT_MONT) ? 1 : 0;
+  HB_DISPATCH_ENC(cfg, k_fore_gradient, l, stream, A)
+  CU(cudaGetLastError());
+  CU(cudaFreeAsync(tbl, stream));
+  return HB_OK;
 }
 
 static int plain_common(hb_ctx* ctx, const uint32_t* a, const uint32_t* b, uint32_t* out, int64_t count,
@@ -272,7 +380,7 @@ int hb_sqrmod(hb_ctx* ctx, const uint32_t* a, uint32_t* out, int64_t count, int 
 }
 
 static int decrypt_common(hb_ctx* ctx, const uint32_t* c, uint32_t* m_out, int64_t count, void* stream_,
-                          uint32_t* tbl_ext) {
+                          uint32_t* tbl_ext, int c_mont = 0) {
   if (!ctx || !c || !m_out) return fail(HB_ERR_ARG, "null pointer");
   if (!ctx->has_private) return fail(HB_ERR_NOPRIVATE, "context has no private key");
   if (count < 0) return fail(HB_ERR_ARG, "negative count");
@@ -283,7 +391,7 @@ static int decrypt_common(hb_ctx* ctx, const uint32_t* c, uint32_t* m_out, int64
   Launch l = plan(ctx, cfg, count);
   const long stride = (long)(ctx->slots_priv + 1) * kCfgs[l.cfg].lpt * 32;
   uint32_t* tbl = tbl_ext;
-  if (!tbl) CU(cudaMallocAsync(&tbl, (size_t)stride * l.nwarps * sizeof(uint32_t), stream));
+  if (!tbl) CU(pool_alloc(ctx->pool, (void**)&tbl, (size_t)stride * l.nwarps * sizeof(uint32_t), stream));
   const uint32_t* base = ctx->d_priv;
   hb::DecArgs A;
   for (int h = 0; h < 2; h++) {
@@ -299,6 +407,7 @@ static int decrypt_common(hb_ctx* ctx, const uint32_t* c, uint32_t* m_out, int64
   A.qR = base + ctx->off_qR;
   A.tbl = tbl; A.tbl_stride = stride; A.stash_slot = ctx->slots_priv;
   A.c = c; A.out = m_out; A.count = count; A.wn = ctx->wn; A.wc = ctx->wc;
+  A.c_mont = c_mont;
   HB_DISPATCH_POW(cfg, k_decrypt, l, stream, A)
   CU(cudaGetLastError());
   if (!tbl_ext) CU(cudaFreeAsync(tbl, stream));
@@ -307,6 +416,27 @@ static int decrypt_common(hb_ctx* ctx, const uint32_t* c, uint32_t* m_out, int64
 
 int hb_decrypt(hb_ctx* ctx, const uint32_t* c, uint32_t* m_out, int64_t count, void* stream) {
   return decrypt_common(ctx, c, m_out, count, stream, nullptr);
+}
+
+int hb_decrypt_rep(hb_ctx* ctx, const uint32_t* c, uint32_t* m_out, int64_t count, int flags, void* stream_) {
+  if (!(flags & HB_A_MONT)) return decrypt_common(ctx, c, m_out, count, stream_, nullptr);
+  if (!ctx || !c || !m_out) return fail(HB_ERR_ARG, "null pointer");
+  if (!ctx->has_private) return fail(HB_ERR_NOPRIVATE, "context has no private key");
+  if (count <= 0) return count == 0 ? HB_OK : fail(HB_ERR_ARG, "negative count");
+  const int Lpub = kCfgs[ctx->cfg_pub].lpt * kCfgs[ctx->cfg_pub].tpi;
+  const int Lpriv = kCfgs[ctx->cfg_priv].lpt * kCfgs[ctx->cfg_priv].tpi;
+  // the kernel reads the digit form directly when the n^2 context's R is the square of the p^2 / q^2 context's
+  // (every standard key size); other shapes go through plain words first
+  if (Lpub == 2 * Lpriv)
+    return decrypt_common(ctx, c, m_out, count, stream_, nullptr, 1);
+  cudaStream_t stream = (cudaStream_t)stream_;
+  CU(cudaSetDevice(ctx->device));
+  uint32_t* words = nullptr;
+  CU(pool_alloc(ctx->pool, (void**)&words, (size_t)count * ctx->wc * sizeof(uint32_t), stream));
+  int rc = hb_ct_convert(ctx, c, words, count, 0, stream_);
+  if (rc == HB_OK) rc = decrypt_common(ctx, words, m_out, count, stream_, nullptr);
+  cudaFreeAsync(words, stream);
+  return rc;
 }
 
 // ---- host-buffer path: pinned staging + two side streams, chunks double-buffered ------------------

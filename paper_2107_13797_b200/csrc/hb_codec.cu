@@ -537,20 +537,15 @@ int hb_decode_f64(hb_ctx* ctx, const uint32_t* m, int exponent, double* values_o
   A.min = m; A.fout = values_out; A.first_bad = (unsigned long long*)first_bad;
   A.maxint_top = ctx->maxint_top;
   cudaStream_t stream = (cudaStream_t)stream_;
+  uint8_t* scratch = nullptr;
   if (ctx->wn % 4 == 0 && ctx->wn >= 8 && ctx->wn <= 128 && ctx->maxint_top >= 3) {
-    if (ctx->codec_cap < (size_t)count + 16) {          // grows rarely; calls on one context use one stream at a time
-      CU(cudaStreamSynchronize(stream));
-      if (ctx->codec_scratch) CU(cudaFree(ctx->codec_scratch));
-      ctx->codec_scratch = nullptr;
-      ctx->codec_cap = 0;
-      const size_t cap = ((size_t)count + 16) * 5 / 4;
-      CU(cudaMalloc(&ctx->codec_scratch, cap));
-      ctx->codec_cap = cap;
-    }
-    uint8_t* slow = ctx->codec_scratch + 16;
+    // marks of the elements left to the generic kernel: per call, from the library's pool (calls on one context
+    // may run on several streams / threads at once)
+    CU(hbi::pool_alloc(ctx->pool, (void**)&scratch, (size_t)count + 16, stream));
+    uint8_t* slow = scratch + 16;
     A.slow = slow;
-    A.nslow = (unsigned long long*)ctx->codec_scratch;
-    CU(cudaMemsetAsync(ctx->codec_scratch, 0, 8, stream));
+    A.nslow = (unsigned long long*)scratch;
+    CU(cudaMemsetAsync(scratch, 0, 8, stream));
     const long warps = (count + 31) / 32;
     const long blocks = std::min<long>((warps + 7) / 8, (long)ctx->sms * 4);
     if (ctx->wn > 64) hb::k_decode_f64_wide<true><<<(unsigned)blocks, 256, 0, stream>>>(A);
@@ -564,6 +559,7 @@ int hb_decode_f64(hb_ctx* ctx, const uint32_t* m, int exponent, double* values_o
   hb::k_decode_f64<<<(unsigned)std::min<long>(tiles, (long)ctx->sms * 16), threads, smem, stream>>>(A);
   g_launches++;
   CU(cudaGetLastError());
+  if (scratch) CU(cudaFreeAsync(scratch, stream));
   return HB_OK;
 }
 

@@ -45,6 +45,11 @@ extern thread_local std::string g_err;
 extern std::atomic<long long> g_launches;
 
 inline int fail(int code, const std::string& msg) { g_err = msg; return code; }
+
+// The library's own stream-ordered memory pool on `device` (one per device and process, shared by the contexts on
+// it).  Scratch never comes from the device's default pool, whose attributes belong to the application.
+cudaMemPool_t device_pool(int device);
+cudaError_t pool_alloc(cudaMemPool_t pool, void** p, size_t bytes, cudaStream_t stream);
 #define CU(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) \
   return hbi::fail(HB_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); } while (0)
 
@@ -103,6 +108,10 @@ inline ModOff add_modulus(ConstBlock& cb, const Big& mod, int L) {
 struct hb_ctx {
   int device = 0;
   int sms = 0;
+  cudaMemPool_t pool = nullptr;       // the library's private stream-ordered pool on this device (hbi::device_pool)
+  int opt_matvec_cbits = 0;           // HB_OPT_MATVEC_WINDOW_BITS: 0 = chosen by row count
+  long opt_matvec_block = 0;          // HB_OPT_MATVEC_BLOCK_ROWS: 0 = 2^21
+  bool sort_smem_set = false;         // k_bucket_sort's dynamic shared-memory limit raised on this device
   int key_bits = 0, wn = 0, wc = 0;
   Big n, n2;
   // public part
@@ -110,17 +119,17 @@ struct hb_ctx {
   uint32_t* d_pub = nullptr;
   hbi::ModOff mod_n2;
   size_t off_nR = 0, off_prog_n = 0;
+  size_t off_nR2 = 0, off_R3 = 0;     // n * R^2 mod n^2, R^3 mod n^2 (Montgomery-form results, see hb_kernels.cuh)
   size_t off_nwords = 0, off_negband = 0, off_maxint = 0, off_n2words = 0;   // n, n - n/3 (wn words); n^2 padded for k_root_inverse
   int nprog_n = 0, slots_n = 0;
   int maxint_top = 0;          // index of the highest non-zero word of max_int = n / 3
-  uint8_t* codec_scratch = nullptr;   // decode: [0, 8) count of elements left to the generic kernel, [16, ..) marks
-  size_t codec_cap = 0;
   int cfg_n = -1;              // limb shape for arithmetic mod n (plaintext side)
   hbi::ModOff mod_n_pub;
   // private part
   bool has_private = false;
   int cfg_priv = -1;
   uint32_t* d_priv = nullptr;
+  size_t priv_bytes = 0;
   struct Half { hbi::ModOff s2, s1; size_t hiR2, hsR, prog; int nprog; } half[2];
   size_t off_qinvR = 0, off_qR = 0;
   hbi::ModOff mod_n_priv;
@@ -176,12 +185,8 @@ constexpr size_t sqr_smem_bytes() { return (size_t)hb::Mont<LPT, TPI>::SQ_WORDS 
 #define HB_SQR_CASE(KERNEL, LPT_, TPI_, launch, stream, args)                                                  \
   {                                                                                                          \
     constexpr size_t smem_ = hbi::sqr_smem_bytes<LPT_, TPI_>();                                              \
-    if (smem_ > 48 * 1024) {                                                                                 \
-      static bool once_ = false;                                                                             \
-      if (!once_) {                                                                                          \
-        CU(cudaFuncSetAttribute(hb::KERNEL<LPT_, TPI_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_)); \
-        once_ = true;                                                                                        \
-      }                                                                                                      \
+    if (smem_ > 48 * 1024) {      /* per device, and cheap: set on every launch of this rarely used path */   \
+      CU(cudaFuncSetAttribute(hb::KERNEL<LPT_, TPI_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_)); \
     }                                                                                                        \
     hb::KERNEL<LPT_, TPI_><<<launch.blocks, launch.threads, smem_, stream>>>(args);                          \
   }                                                                                                          \

@@ -85,9 +85,28 @@ __device__ __forceinline__ uint32_t* sqr_scratch() {
   }
 }
 
+// Representation of a ciphertext array crossing a kernel boundary (include/hebatch_b200.h, HB_REP_*): plain
+// little-endian words (wc per element, the HAFB payload) or Montgomery digit form x * R mod n^2 (L limbs per
+// element), the form chained operators keep on the device.  Multiplying a Montgomery operand by a plain one yields
+// a plain product, two Montgomery operands a Montgomery product: an operator whose inputs are resident costs no
+// conversion.
+template <int LPT, int TPI>
+__device__ __forceinline__ void load_ct(const Mont<LPT, TPI>& mt, uint32_t (&x)[LPT], const uint32_t* base, long i,
+                                        int wc, int mont) {
+  if (mont) mt.load_limbs(x, base + i * (LPT * TPI));
+  else mt.load_words(x, base + i * wc, wc);
+}
+template <int LPT, int TPI>
+__device__ __forceinline__ void store_ct(const Mont<LPT, TPI>& mt, uint32_t* base, long i, int wc, int mont,
+                                         const uint32_t (&x)[LPT], bool valid) {
+  if (mont) { if (valid) mt.store_limbs(base + i * (LPT * TPI), x); }
+  else mt.store_words(base + i * wc, wc, x, valid);
+}
+
 struct EncArgs {
   ModDev mod;                // n^2
-  const uint32_t* nR;        // n * R mod n^2 : mul(m, nR) = m*n
+  const uint32_t* nR;        // n * R mod n^2 : mul(m, nR) = m*n            (n * R^2 when out_mont: m*n*R)
+  int c_mont, out_mont;      // representation of c (mode 1) and of the result
   const uint32_t* prog;      // exponent n
   int nprog;
   uint32_t* tbl;             // per-warp scratch tiles
@@ -127,20 +146,130 @@ __global__ void __launch_bounds__(32, 4 * blocks_per_sm(LPT)) k_encrypt(EncArgs 
       uint32_t z[LPT];
       mt.load_words(y, A.m + ii * A.wn, A.wn);
       mt.load_limbs(z, A.nR);
-      mt.mul(y, y, z);                            // m*n (plain)
-      mt.set_one(z);
+      mt.mul(y, y, z);                            // m*n, in the representation the result is wanted in
+      if (A.out_mont) mt.load_limbs(z, A.mod.r1); else mt.set_one(z);
       mt.add_mod(y, y, z);                        // 1 + m*n  (< n^2, nothing is reduced)
     } else {
-      mt.load_words(y, A.c + ii * A.wc, A.wc);
+      load_ct<LPT, TPI>(mt, y, A.c, ii, A.wc, A.c_mont);
+      if (A.c_mont != A.out_mont) {               // one conversion so that Mont(r^n) * y lands in the wanted form
+        uint32_t z[LPT];
+        if (A.out_mont) mt.load_limbs(z, A.mod.r2); else mt.set_one(z);
+        mt.mul(y, y, z);
+      }
     }
-    mt.mul(x, x, y);                              // plain product, canonical
-    mt.store_words(A.out + ii * A.wc, A.wc, x, valid);
+    mt.mul(x, x, y);                              // canonical
+    store_ct<LPT, TPI>(mt, A.out, ii, A.wc, A.out_mont, x, valid);
+  }
+}
+
+// Fused fore-gradient chain of one heterogeneous-FLR mini-batch (reference arena.py:345-366, the cached pipeline
+// plain_mul -> encrypt -> hmul -> hadd -> plain_mul -> hadd(lifted plaintext)), one pass per element:
+//     out = (1 + (lg * kg mod n) n) r^n  *  c^kh  *  (1 + yl n)      mod n^2
+// lg: the guest's logits (plaintext residues), kg: the plaintext factor (encode(0.25) -> 4) as a residue, c: the
+// host's encrypted logits, kh: the same factor as a small positive exponent, yl: the label term already multiplied
+// and re-gridded on the plaintext side (hb_plain_mulmod, hb_plain_rescale -- which also own the overflow checks).
+// Every factor is an exact residue, so the bits equal the reference's six-operator sequence.  n (x mod n) = n x mod
+// n^2, hence lg * kg needs no reduction mod n of its own: one multiplication by kg n R^2.
+struct ForeArgs {
+  ModDev mod;                // n^2
+  const uint32_t* nR2;       // n * R^2 mod n^2
+  const uint32_t* prog;      // exponent n
+  int nprog;
+  uint32_t* tbl;             // per-warp scratch tiles; slots `spare` and `spare + 1` are this kernel's
+  long tbl_stride;
+  int spare;
+  const uint32_t* lg;        // wn words each
+  const uint32_t* kg;        // wn words (one residue)
+  const uint32_t* c;         // ciphertexts
+  const uint32_t* yl;        // wn words each
+  const uint32_t* r;         // obfuscation factors, wn words each
+  uint32_t* out;
+  uint32_t kh;               // exponent for c, >= 1
+  long count;
+  int wn, wc;
+  int c_mont, out_mont;
+};
+
+template <int LPT, int TPI>
+__global__ void __launch_bounds__(32, 4 * blocks_per_sm(LPT)) k_fore_gradient(ForeArgs A) {
+  using M = Mont<LPT, TPI>;
+  constexpr int IPW = 32 / TPI;
+  M mt;
+  mt.init(A.mod.n, A.mod.np);
+  const int lane = threadIdx.x, g = lane / TPI;
+  const long wg = blockIdx.x, nw = gridDim.x;
+  uint32_t* tw = A.tbl + wg * A.tbl_stride;
+  uint32_t* sw = sqr_scratch<LPT, TPI>();
+  {
+    uint32_t x[LPT], y[LPT];
+    mt.load_words(x, A.kg, A.wn);
+    mt.load_limbs(y, A.nR2);
+    mt.mul(x, x, y);                              // kg n R
+    mt.load_limbs(y, A.mod.r2);
+    mt.mul(x, x, y);                              // kg n R^2 : mul(lg, .) = Mont(lg kg n)
+    tile_store<LPT>(tw, A.spare, x);
+  }
+  const int htop = 31 - __clz(A.kh | 1u);
+  const long ntiles = (A.count + IPW - 1) / IPW;
+  for (long tile = wg; tile < ntiles; tile += nw) {
+    long inst = tile * IPW + g;
+    bool valid = inst < A.count;
+    long ii = valid ? inst : A.count - 1;
+    uint32_t x[LPT], y[LPT];
+    // c^kh, left to right (kh is a launch constant: uniform control flow)
+    load_ct<LPT, TPI>(mt, y, A.c, ii, A.wc, A.c_mont);
+    if (!A.c_mont) {
+      mt.load_limbs(x, A.mod.r2);
+      mt.mul(y, y, x);
+    }
+#pragma unroll
+    for (int k = 0; k < LPT; k++) x[k] = y[k];
+#pragma unroll 1
+    for (int b = htop - 1; b >= 0; b--) {
+      uint32_t z[LPT];
+#pragma unroll
+      for (int k = 0; k < LPT; k++) z[k] = x[k];
+      mt.mul(x, x, z);
+      if ((A.kh >> b) & 1u) mt.mul(x, x, y);
+    }
+    tile_store<LPT>(tw, A.spare + 1, x);
+    mt.load_words(x, A.r + ii * A.wn, A.wn);
+    mt.load_limbs(y, A.mod.r2);
+    mt.mul(x, x, y);                              // Mont(r)
+    run_prog<LPT, TPI>(mt, x, A.prog, A.nprog, tw, sw);  // Mont(r^n)
+    {
+      uint32_t z[LPT];
+      mt.load_words(y, A.lg + ii * A.wn, A.wn);
+      tile_load<LPT>(tw, A.spare, z);
+      mt.mul(y, y, z);
+      mt.load_limbs(z, A.mod.r1);
+      mt.add_mod(y, y, z);                        // Mont(1 + (lg kg mod n) n)
+    }
+    mt.mul(x, x, y);                              // Mont(encrypted guest term)
+    tile_load<LPT>(tw, A.spare + 1, y);
+    mt.mul(x, x, y);                              // * c^kh
+    {
+      uint32_t z[LPT];
+      mt.load_words(y, A.yl + ii * A.wn, A.wn);
+      mt.load_limbs(z, A.nR2);
+      mt.mul(y, y, z);
+      mt.load_limbs(z, A.mod.r1);
+      mt.add_mod(y, y, z);                        // Mont(1 + yl n)
+    }
+    mt.mul(x, x, y);
+    if (!A.out_mont) {
+      mt.set_one(y);
+      mt.mul(x, x, y);
+    }
+    store_ct<LPT, TPI>(mt, A.out, ii, A.wc, A.out_mont, x, valid);
   }
 }
 
 struct MulArgs {
   ModDev mod;
-  const uint32_t* nR;
+  const uint32_t* nR;     // n * R mod n^2
+  const uint32_t* nR2;    // n * R^2 mod n^2
+  const uint32_t* r3;     // R^3 mod n^2
   const uint32_t* a;
   const uint32_t* b;      // ciphertexts (lift == 0) or plaintext residues (lift == 1)
   uint32_t* out;
@@ -148,6 +277,7 @@ struct MulArgs {
   int wn, wc;
   int lift;
   int b_broadcast;
+  int a_mont, b_mont, out_mont;
 };
 
 template <int LPT, int TPI>
@@ -167,20 +297,30 @@ __global__ void __launch_bounds__(32, 4 * blocks_per_sm(LPT)) k_mulmod(MulArgs A
     long ii = valid ? inst : A.count - 1;
     long ib = A.b_broadcast ? 0 : ii;
     uint32_t x[LPT], y[LPT];
+    // power of R carried by a * b / R:  rep(a) + rep(b) - 1  with Montgomery = 1, plain = 0
+    int rb = A.b_mont;
     if (A.lift) {
+      // 1 + m n costs the same in either form: take the one that makes the product land where it is wanted
+      rb = (A.a_mont == A.out_mont) ? 1 : 0;
+      if (!A.a_mont && A.out_mont) rb = 1;
       mt.load_words(x, A.b + ib * A.wn, A.wn);
-      mt.load_limbs(y, A.nR);
+      mt.load_limbs(y, rb ? A.nR2 : A.nR);
       mt.mul(y, x, y);                            // m*n
-      mt.set_one(x);
+      if (rb) mt.load_limbs(x, A.mod.r1); else mt.set_one(x);
       mt.add_mod(y, y, x);                        // 1 + m*n
     } else {
-      mt.load_words(y, A.b + ib * A.wc, A.wc);
+      load_ct<LPT, TPI>(mt, y, A.b, ib, A.wc, A.b_mont);
     }
-    mt.load_limbs(x, A.mod.r2);
-    mt.mul(y, y, x);                              // Mont(b)
-    mt.load_words(x, A.a + ii * A.wc, A.wc);
-    mt.mul(x, x, y);                              // a*b plain, canonical
-    mt.store_words(A.out + ii * A.wc, A.wc, x, valid);
+    load_ct<LPT, TPI>(mt, x, A.a, ii, A.wc, A.a_mont);
+    mt.mul(x, x, y);
+    const int got = A.a_mont + rb - 1;            // -1, 0 or 1
+    if (got != A.out_mont) {                      // one multiplication by R^(out - got + 1)
+      const int e = A.out_mont - got + 1;         // 0, 2 or 3
+      if (e == 0) mt.set_one(y);
+      else mt.load_limbs(y, e == 2 ? A.mod.r2 : A.r3);
+      mt.mul(x, x, y);
+    }
+    store_ct<LPT, TPI>(mt, A.out, ii, A.wc, A.out_mont, x, valid);
   }
 }
 
@@ -294,6 +434,7 @@ struct DecArgs {
   uint32_t* out;
   long count;
   int wn, wc;
+  int c_mont;                // c is in Montgomery digit form of the n^2 context, whose R is the square of this one's
 };
 
 template <int LPT, int TPI>
@@ -313,19 +454,29 @@ __global__ void __launch_bounds__(32, 4 * blocks_per_sm(LPT)) k_decrypt(DecArgs 
     long inst = tile * IPW + g;
     bool valid = inst < A.count;
     long ii = valid ? inst : A.count - 1;
-    const uint32_t* cw = A.c + ii * A.wc;
+    // Montgomery input: 2 L limbs v = vlo + vhi R' with v = c R'^2 mod n^2, so Mont'(c mod s^2) = vlo / R' + vhi
+    const uint32_t* cw = A.c + ii * (A.c_mont ? 2 * LPT * TPI : A.wc);
     uint32_t x[LPT], y[LPT], z[LPT];
 #pragma unroll 1
     for (int h = 0; h < 2; h++) {
       const HalfDev& H = A.half[h];
       mt.init(H.s2.n, H.s2.np);
-      // c mod s^2 in Montgomery form, from the two word halves of c
-      mt.load_words(x, cw, wlo);
-      mt.load_limbs(y, H.s2.r2);
-      mt.mul(x, x, y);
-      mt.load_words(y, cw + wlo, whi);
-      mt.load_limbs(z, H.hiR2);
-      mt.mul(y, y, z);
+      // c mod s^2 in Montgomery form, from the two halves of c
+      if (A.c_mont) {
+        mt.load_limbs(x, cw);
+        mt.set_one(y);
+        mt.mul(x, x, y);                            // vlo / R' mod s^2
+        mt.load_limbs(y, cw + LPT * TPI);
+        mt.load_limbs(z, H.s2.r1);
+        mt.mul(y, y, z);                            // vhi mod s^2
+      } else {
+        mt.load_words(x, cw, wlo);
+        mt.load_limbs(y, H.s2.r2);
+        mt.mul(x, x, y);
+        mt.load_words(y, cw + wlo, whi);
+        mt.load_limbs(z, H.hiR2);
+        mt.mul(y, y, z);
+      }
       mt.add_mod(x, x, y);
       run_prog<LPT, TPI>(mt, x, H.prog, H.nprog, tw, sw);   // Mont(c^(s-1) mod s^2)
       mt.set_one(z);

@@ -282,7 +282,8 @@ struct ScalarPrepArgs {
 
 __global__ void k_scalar_prep(ScalarPrepArgs A) {
   long e = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= A.nscal) return;
+  const bool live = e < A.nscal;
+  if (!live) e = A.nscal - 1;
   const uint32_t* k = A.k + e * A.wn;
   // k > negband ?
   int cmp = 0;
@@ -309,10 +310,68 @@ __global__ void k_scalar_prep(ScalarPrepArgs A) {
   }
   long o = e;
   if (A.transpose) { long r = e / A.cols, c = e - r * A.cols; o = c * A.rows + r; }
-  A.mag64[o] = lo;
-  A.neg[o] = neg ? 1 : 0;
-  atomicMax(A.maxbits, bits);
-  if (neg) atomicAdd(A.nneg, 1);
+  if (live) {
+    A.mag64[o] = lo;
+    A.neg[o] = neg ? 1 : 0;
+  }
+  // one atomic per warp, not per scalar (2e8 scalars at BASELINE configs[3])
+  const int wbits = __reduce_max_sync(0xffffffffu, live ? bits : 0);
+  const int wneg = __popc(__ballot_sync(0xffffffffu, live && neg));
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(A.maxbits, wbits);
+    if (wneg) atomicAdd(A.nneg, wneg);
+  }
+}
+
+// The same compact form straight from doubles (encoding.py:54-78 with a target exponent): the feature matrices of a
+// federated run never need their 256-byte residues -- hb_matvec only reads sign and magnitude.  info[0] = max bit
+// length, info[1] = negatives, info[2] = values whose magnitude does not fit 64 bits (the caller then encodes full
+// residues instead).  Rounding is round-half-even on the exact binary value, like k_encode_f64.
+struct CompactEncArgs {
+  const double* values; long nscal; long rows, cols; int exponent;
+  uint64_t* mag64; uint8_t* neg; int* info;
+};
+
+__global__ void k_encode_compact(CompactEncArgs A) {
+  long e = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = e < A.nscal;
+  if (!live) e = A.nscal - 1;
+  const unsigned long long bits = (unsigned long long)__double_as_longlong(A.values[e]);
+  const bool negv = (bits >> 63) != 0;
+  const int e11 = (int)((bits >> 52) & 0x7ff);
+  unsigned long long mant = bits & 0xfffffffffffffull;
+  int e2;
+  if (e11 == 0) e2 = -1074; else { mant |= 1ull << 52; e2 = e11 - 1075; }
+  long shift = (long)e2 - 4L * A.exponent;        // scaled = mant * 2^shift
+  bool wide = e11 == 0x7ff;                        // non-finite: never compact
+  if (shift < 0) {
+    const long s = -shift;
+    if (s >= 64) mant = 0;
+    else {
+      unsigned long long q = mant >> s, rem = mant & ((1ull << s) - 1ull), half = 1ull << (s - 1);
+      if (rem > half || (rem == half && (q & 1ull))) q++;
+      mant = q;
+    }
+    shift = 0;
+  }
+  int nb = mant ? 64 - __clzll(mant) : 0;
+  if (mant && nb + shift > 64) wide = true;
+  const unsigned long long mag = (mant && !wide) ? (mant << shift) : 0ull;
+  nb = (mant && !wide) ? nb + (int)shift : 0;
+  const bool neg = negv && mag != 0;
+  const long r = e / A.cols, c = e - r * A.cols;
+  if (live) {
+    A.mag64[c * A.rows + r] = mag;
+    A.neg[c * A.rows + r] = neg ? 1 : 0;
+  }
+  const int wbits = __reduce_max_sync(0xffffffffu, live ? nb : 0);
+  const int wneg = __popc(__ballot_sync(0xffffffffu, live && neg));
+  const int wwide = __popc(__ballot_sync(0xffffffffu, live && wide));
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(A.info, wbits);
+    if (wneg) atomicAdd(A.info + 1, wneg);
+    if (wwide) atomicAdd(A.info + 2, wwide);
+  }
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -334,9 +393,10 @@ struct PowVarArgs {
   int ebits;                 // exponent bits to process (multiple of win)
   int win;                   // window bits (1..4)
   uint32_t* tbl; long tbl_stride;
-  uint32_t* out;             // words (wc each)
+  uint32_t* out;             // words (wc each), or digit form when out_mont
   int wc;
   long count;
+  int out_mont;
 };
 
 template <int LPT, int TPI>
@@ -410,9 +470,29 @@ __global__ void __launch_bounds__(32, 4 * blocks_per_sm(LPT)) k_powvar(PowVarArg
       for (int k = 0; k < LPT; k++) y[k] = tw[((int)d * LPT + k) * 32 + ln];
       mt.mul(x, x, y);
     }
-    mt.set_one(y);
-    mt.mul(x, x, y);
-    mt.store_words(A.out + e * A.wc, A.wc, x, valid);
+    if (A.out_mont) {
+      if (valid) mt.store_limbs(A.out + e * L, x);
+    } else {
+      mt.set_one(y);
+      mt.mul(x, x, y);
+      mt.store_words(A.out + e * A.wc, A.wc, x, valid);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// Bases whose inverse is needed: sel[i] = cm[i] when one of the scalars paired with base i is negative, Mont(1)
+// otherwise -- so that a non-unit ciphertext only fails the batch inversion when the reference would invert it too
+// (operators.py:60-61 inverts per element).  Base i meets the scalars k[(i * c_div + j) % k_period], j < c_div.
+struct MaskArgs { const uint32_t* cm; const uint32_t* one; const uint8_t* neg; long nbase; long c_div; long k_period; int L; uint32_t* sel; };
+
+__global__ void k_mask_bases(MaskArgs A) {
+  const long total = A.nbase * A.L;
+  for (long idx = (long)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += (long)gridDim.x * blockDim.x) {
+    const long i = idx / A.L; const int k = (int)(idx - i * A.L);
+    bool need = false;
+    for (long j = 0; j < A.c_div && !need; j++) need = A.neg[(i * A.c_div + j) % A.k_period] != 0;
+    A.sel[idx] = need ? A.cm[idx] : A.one[k];
   }
 }
 
@@ -428,6 +508,8 @@ struct ProductArgs {
   long ngroups, glen, gstride, estride;
   long parts, clen;
   uint32_t* out;
+  int in_mont;              // inputs are digit form (L limbs each): no deficit to repair
+  int out_mont;             // write digit form
 };
 
 template <int LPT, int TPI>
@@ -437,13 +519,15 @@ __global__ void __launch_bounds__(32, 4 * blocks_per_sm(LPT)) k_product_pass(Pro
   mt.init(A.mod.n, A.mod.np);
   const long nitems = A.ngroups * A.parts;
   const long ntiles = (nitems + IPW - 1) / IPW;
-  // fix = R^clen mod n :  h_j = R^(j+1), mul(h_a, h_b) = h_(a+b); we need h_(clen-1)
+  // Plain inputs leave x = prod / R^(clen-1): one multiplication by R^(clen + out_mont) repairs it.
+  // h_j = R^(j+1), mul(h_a, h_b) = h_(a+b): built left to right below; we need h_(clen + out_mont - 1).
+  // Digit-form inputs carry no deficit: Mont(prod) is already there (multiplied by one when plain words are wanted).
   uint32_t fix[LPT];
-  {
+  if (!A.in_mont) {
     uint32_t h1[LPT];
     mt.load_limbs(fix, A.mod.r1);     // h_0
     mt.load_limbs(h1, A.mod.r2);      // h_1
-    long idx = A.clen - 1;
+    long idx = A.clen - 1 + A.out_mont;
     int top = 63 - __clzll((unsigned long long)(idx | 1));
 #pragma unroll 1
     for (int b = top; b >= 0; b--) {
@@ -463,7 +547,10 @@ __global__ void __launch_bounds__(32, 4 * blocks_per_sm(LPT)) k_product_pass(Pro
 #pragma unroll 1
     for (long i = 0; i < A.clen; i++) {
       long t = t0 + i;
-      if (t < A.glen) mt.load_words(y, A.c + (grp * A.gstride + t * A.estride) * A.win, A.win);
+      if (t < A.glen) {
+        if (A.in_mont) mt.load_limbs(y, A.c + (grp * A.gstride + t * A.estride) * L);
+        else mt.load_words(y, A.c + (grp * A.gstride + t * A.estride) * A.win, A.win);
+      } else if (A.in_mont) mt.load_limbs(y, A.mod.r1);
       else mt.set_one(y);
       if (first) {
 #pragma unroll
@@ -473,8 +560,14 @@ __global__ void __launch_bounds__(32, 4 * blocks_per_sm(LPT)) k_product_pass(Pro
         mt.mul(x, x, y);
       }
     }
-    mt.mul(x, x, fix);      // clen - 1 deficits repaired: x * R^clen / R
-    mt.store_words(A.out + it * A.wc, A.wc, x, valid);
+    if (!A.in_mont) {
+      mt.mul(x, x, fix);    // clen - 1 deficits repaired: x * R^(clen + out_mont) / R
+    } else if (!A.out_mont) {
+      mt.set_one(y);
+      mt.mul(x, x, y);
+    }
+    if (A.out_mont) { if (valid) mt.store_limbs(A.out + it * L, x); }
+    else mt.store_words(A.out + it * A.wc, A.wc, x, valid);
   }
 }
 
@@ -484,8 +577,9 @@ __global__ void __launch_bounds__(32, 4 * blocks_per_sm(LPT)) k_product_pass(Pro
 // list are multiplied up by one group each; per-bucket products are combined and folded with the
 // running-sum identity  prod_v B_v^v = prod_v (prod_{u>=v} B_u); windows are merged by Horner.
 struct SortArgs {
-  const uint64_t* mag64;   // [d][n]
-  const uint8_t* neg;      // [d][n]
+  const uint64_t* mag64;   // [d][colstride], the n rows of this call starting at the pointer
+  const uint8_t* neg;      // same layout
+  long colstride;          // rows of the whole matrix (>= n when the call covers a block of rows)
   long n; int d; int nwin; int cbits;
   uint32_t* boff;          // [d][nwin][NB + 1] exclusive offsets
   uint32_t* sorted;        // [d][nwin][n]   rows ordered by bucket (boff delimits the buckets)
@@ -498,8 +592,8 @@ __global__ void __launch_bounds__(256) k_bucket_sort(SortArgs A) {
   uint32_t* cur = hist + NB + 1;
   for (int i = threadIdx.x; i <= NB; i += blockDim.x) hist[i] = 0;
   __syncthreads();
-  const uint64_t* mg = A.mag64 + (long)j * A.n;
-  const uint8_t* ng = A.neg + (long)j * A.n;
+  const uint64_t* mg = A.mag64 + (long)j * A.colstride;
+  const uint8_t* ng = A.neg + (long)j * A.colstride;
   const uint32_t vmask = (1u << A.cbits) - 1u;
   const int sh = w * A.cbits;
   for (long t = threadIdx.x; t < A.n; t += blockDim.x) {
@@ -821,7 +915,7 @@ __global__ void __launch_bounds__(32, 4 * blocks_per_sm(LPT)) k_fold(FoldArgs A)
 }
 
 // out_j = A_j * Binv_j  ->  plain words
-struct FinishArgs { ModDev mod; const uint32_t* ab; const uint32_t* binv; int d; uint32_t* out; int wc; };
+struct FinishArgs { ModDev mod; const uint32_t* ab; const uint32_t* binv; int d; uint32_t* out; int wc; int out_mont; };
 
 template <int LPT, int TPI>
 __global__ void __launch_bounds__(32, 4 * blocks_per_sm(LPT)) k_matvec_finish(FinishArgs A) {
@@ -839,9 +933,13 @@ __global__ void __launch_bounds__(32, 4 * blocks_per_sm(LPT)) k_matvec_finish(Fi
       mt.load_limbs(y, A.binv + j * L);
       mt.mul(x, x, y);
     }
-    mt.set_one(y);
-    mt.mul(x, x, y);
-    mt.store_words(A.out + j * A.wc, A.wc, x, valid);
+    if (A.out_mont) {
+      if (valid) mt.store_limbs(A.out + j * L, x);
+    } else {
+      mt.set_one(y);
+      mt.mul(x, x, y);
+      mt.store_words(A.out + j * A.wc, A.wc, x, valid);
+    }
   }
 }
 

@@ -77,8 +77,8 @@ def batch_encode(pk: PublicKey, values, exponent: int, backend: ExecutionBackend
     if vals.shape[0] == 0:
         return PlaintextBatch(pk, (0,), (exponent or 0,), (), True)
     be = _cuda(backend)
-    words = be.encode_f64(pk.n, vals, exponent)        # exponent None (used by encode_batch): exact shared exponent
-    return PlaintextBatch(pk, (vals.shape[0],), (be.last_exponent,), words, True)
+    words, used = be.encode_f64(pk.n, vals, exponent)  # exponent None (used by encode_batch): exact shared exponent
+    return PlaintextBatch(pk, (vals.shape[0],), (used,), words, True)
 
 
 def batch_decode(pk: PublicKey, batch: PlaintextBatch, backend: ExecutionBackend | None = None) -> list:
@@ -170,7 +170,7 @@ def batch_add(pk: PublicKey, a: CiphertextBatch, b, backend: ExecutionBackend | 
             raise ExponentMismatch(
                 f"plaintext exponent {b.exponents[0]} finer than ciphertext {target}; "
                 "encode the ciphertext side at least as fine")
-        b = plain_rescale(b, target)
+        b = plain_rescale(b, target, be)
         out = be.lift_mulmod(pk.n, a.words, b.words, broadcast) if a.count else a.words
         return CiphertextBatch(pk, a.shape, a.exponents, out, a.shared_exponent, a.obfuscated)
     if a.shape != b.shape:

@@ -1,4 +1,6 @@
-"""Multi-GPU execution of the operators: one process per GPU, `torch.distributed` for the plumbing.
+"""Multi-GPU execution of the operators, SPMD form: one process per GPU, `torch.distributed` for the plumbing.
+(The single-process form -- one backend driving every device of the box, which is what the sequential FLR parties
+need -- is backends.MultiDeviceBackend; both use the same partial / combine kernels.)
 
 Element-wise operators (encrypt, obfuscate, decrypt, add, mul) shard by contiguous element ranges of
 ceil(count / world) -- the reference's own schedule (backends.py:64-73 of the reference) -- and need no
@@ -18,17 +20,9 @@ from __future__ import annotations
 
 import numpy as np
 
+from .backends import shard_range      # noqa: F401  (the reference's ceil(count / workers) schedule)
 from .batches import CiphertextBatch, PlaintextBatch, ShapeMismatch, ct_width, shared_exponent_of
 from .device import WordArray
-
-
-def shard_range(count: int, rank: int, world: int) -> tuple:
-    """[lo, hi) of rank's contiguous slice; chunks of ceil(count / world), the last ones possibly empty."""
-    if world < 1 or not 0 <= rank < world:
-        raise ValueError("bad rank / world")
-    chunk = -(-count // world) if count else 0
-    lo = min(rank * chunk, count)
-    return lo, min(lo + chunk, count)
 
 
 def shard_rows(batch, rank: int, world: int):

@@ -612,11 +612,27 @@ def test_default_exponent_found_on_the_device(okeys):
     assert encode_batch(pk, []).exponents == (0,)
 
 
+@pytest.fixture
+def forced_window(okeys):
+    """hb_ctx_set_option(HB_OPT_MATVEC_WINDOW_BITS) on the contexts of the keys a test uses, reset afterwards."""
+    from paper_2107_13797_b200.backends import default_backend
+    touched = []
+
+    def force(bits, names):
+        for name in names:
+            n = okeys(name).n
+            default_backend().set_matvec_window(n, bits)
+            touched.append(n)
+    yield force
+    for n in touched:
+        default_backend().set_matvec_window(n, 0)
+
+
 @pytest.mark.parametrize("width", ["9", "11", "13"])
-def test_matmul_wide_windows(okeys, monkeypatch, width):
+def test_matmul_wide_windows(okeys, forced_window, width):
     """The bucket matvec with the window widths tall matrices use (9 bits from 32 k rows, 13 bits with the
     piecewise fold from 200 k rows), forced here on small problems: same bits as the oracle."""
-    monkeypatch.setenv("HB_MATVEC_CBITS", width)
+    forced_window(int(width), ("k128", "k512", "k1024"))
     for name in ("k128", "k1024"):
         test_matmul(okeys, name)
     test_matmul_wide(okeys)

@@ -13,7 +13,7 @@ import torch.multiprocessing as mp
 import hebatch_oracle as ho
 from paper_2107_13797_b200 import paillier, sharding
 from paper_2107_13797_b200.batches import CiphertextBatch, PlaintextBatch
-from paper_2107_13797_b200.device import WordArray, words_to_ints
+from paper_2107_13797_b200.device import WordArray
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -44,52 +44,72 @@ def test_shard_rows_keeps_metadata():
     assert [p.exponents for p in parts] == [(0, 1, 2, 3), (4, 5)] and parts[1].shape == (1, 2)
 
 
+class IntBackend:
+    """Stands in for the device kernels behind sharding.sharded_matmul / sharded_sum with the oracle's integer
+    arithmetic, so that the REAL gather / combine code of sharding.py runs with two processes on CPU."""
+
+    def __init__(self, ok):
+        self.ok = ok
+        self.wc = ((2 * ok.key_bits + 7) // 8 + 3) // 4
+
+    def matvec_partial(self, n, c, k, inner, d):
+        ok = self.ok
+        cs, ks = c.ints(), k.ints()
+        pairs = []
+        for j in range(d):
+            a = b = 1
+            for t in range(inner):
+                kk = ks[t * d + j]
+                if kk > ok.neg_band:
+                    b = b * pow(cs[t], ok.n - kk, ok.n2) % ok.n2
+                else:
+                    a = a * pow(cs[t], kk, ok.n2) % ok.n2
+            pairs += [a, b]
+        return WordArray.from_ints(pairs, self.wc)
+
+    def matvec_combine(self, n, ab_all, nranks, d):
+        flat = ab_all.ints()
+        blocks = [[(flat[(r * d + j) * 2], flat[(r * d + j) * 2 + 1]) for j in range(d)] for r in range(nranks)]
+        return WordArray.from_ints(sharding.combine_partials_reference(self.ok.n2, blocks), self.wc)
+
+    def product(self, n, c, ngroups, glen, gstride, estride):
+        assert ngroups == 1 and estride == 1
+        tot = 1
+        for v in c.ints()[:glen]:
+            tot = tot * v % self.ok.n2
+        return WordArray.from_ints([tot], self.wc)
+
+
 def _worker(rank, world, port, ret):
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import torch
     import torch.distributed as dist
+    from paper_2107_13797_b200 import operators
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         ok = ho.keygen(128, random.Random(1234))
+        pk = paillier.PublicKey(ok.n)
+        be = IntBackend(ok)
+        operators._cuda = lambda backend: backend          # the stub is not a CudaBackend; nothing else changes
         rng = random.Random(7)
         inner, d = 11, 3
         ms = [rng.randrange(ok.n) for _ in range(inner)]
         rs = [ho.draw_unit(ok.n, rng) for _ in ms]
         cs = ho.k_encrypt(ok, list(zip(ms, rs)))
         ks = [rng.getrandbits(30) if i % 2 else ok.n - rng.getrandbits(30) for i in range(inner * d)]
-        lo, hi = sharding.shard_range(inner, rank, world)
-        # this rank's partial pairs (A_j, B_j), computed on integers in place of hb_matvec_partial
-        pairs = []
-        for j in range(d):
-            a = b = 1
-            for t in range(lo, hi):
-                k = ks[t * d + j]
-                if k > ok.neg_band:
-                    b = b * pow(cs[t], ok.n - k, ok.n2) % ok.n2
-                else:
-                    a = a * pow(cs[t], k, ok.n2) % ok.n2
-            pairs += [a, b]
-        wc = ((2 * ok.key_bits + 7) // 8 + 3) // 4
-        local = WordArray.from_ints(pairs, wc)
-        gathered = sharding.all_gather_words(sharding._comm_tensor(local, None))
-        assert tuple(gathered.shape) == (world, 2 * d, wc)
-        flat = words_to_ints(gathered.reshape(world * 2 * d, wc).numpy().view(np.uint32))
-        blocks = [[(flat[(r * d + j) * 2], flat[(r * d + j) * 2 + 1]) for j in range(d)] for r in range(world)]
-        got = sharding.combine_partials_reference(ok.n2, blocks)
+        a = CiphertextBatch(pk, (inner,), (-3,), cs, True, obfuscated=True)
+        x = PlaintextBatch(pk, (inner, d), (-2,), ks, True)
+        # the product's own sharding helpers, then the product's own gather + combine
+        a_loc, x_loc = sharding.shard_rows(a, rank, world), sharding.shard_rows(x, rank, world)
+        got = sharding.sharded_matmul(pk, a_loc, x_loc, be)
         cols = tuple(tuple(ks[t * d + j] for t in range(inner)) for j in range(d))
         want = ho.k_dot(ok, (tuple(cs),), cols, [(0, j) for j in range(d)])
-        # the sum: per-rank partial products, gathered, multiplied
-        part = 1
-        for c in cs[lo:hi]:
-            part = part * c % ok.n2
-        g2 = sharding.all_gather_words(sharding._comm_tensor(WordArray.from_ints([part], wc), None))
-        tot = 1
-        for v in words_to_ints(g2.reshape(world, wc).numpy().view(np.uint32)):
-            tot = tot * v % ok.n2
-        ret[rank] = (got == want, tot == ho.k_product(ok, [cs])[0], (lo, hi))
+        ok_mat = (list(got.payload) == want and got.exponents == (-5,) and got.shape == (d,) and got.obfuscated)
+        total = sharding.sharded_sum(pk, a_loc, be)
+        ok_sum = list(total.payload) == ho.k_product(ok, [cs]) and total.exponents == (-3,)
+        ret[rank] = (ok_mat, ok_sum, (a_loc.count, x_loc.shape))
     finally:
         dist.destroy_process_group()
 
@@ -102,4 +122,4 @@ def test_two_rank_gather_and_combine():
     ret = mgr.dict()
     mp.spawn(_worker, args=(2, port, ret), nprocs=2, join=True)
     assert ret[0][:2] == (True, True) and ret[1][:2] == (True, True)
-    assert ret[0][2] == (0, 6) and ret[1][2] == (6, 11)
+    assert ret[0][2] == (6, (6, 3)) and ret[1][2] == (5, (5, 3))
