@@ -28,3 +28,24 @@ def test_other_ranks_of_the_reference_arm_do_nothing():
                           "--steps", "1", "--warmup", "0", "--cpu-sample", "32"], capture_output=True, text=True,
                          timeout=120, cwd=ROOT, env=env)
     assert res.returncode == 0 and res.stdout.strip() == ""
+
+
+def test_gpus_flag_respawns_one_rank_per_gpu(monkeypatch):
+    """`python bench.py --gpus N` without a launcher re-executes itself under torch.distributed.run with N ranks on
+    127.0.0.1 (the driver's own launch line); under a launcher (WORLD_SIZE set) it does not."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    seen = {}
+    monkeypatch.setattr(bench.subprocess, "call", lambda cmd: seen.setdefault("cmd", cmd) and 0)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "2", "--warmup", "3"])
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    try:
+        bench.main()
+    except SystemExit as exc:
+        assert exc.code == 0
+    cmd = seen["cmd"]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"] and "--nproc-per-node=4" in cmd
+    assert cmd[cmd.index("--master-addr") + 1] == "127.0.0.1"
+    assert cmd[-6:] == ["--gpus", "4", "--steps", "2", "--warmup", "3"]

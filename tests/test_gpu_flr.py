@@ -29,7 +29,7 @@ def run_case(case):
     return fed, results, time.time() - t0
 
 
-@pytest.mark.parametrize("name", ["small_uncached", "config1"])
+@pytest.mark.parametrize("name", ["small_uncached", "config1", "full_batch_2048x200"])
 def test_hetero_flr_equals_reference(name):
     case = GOLD[name]
     fed, results, secs = run_case(case)

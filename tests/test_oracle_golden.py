@@ -141,7 +141,7 @@ def _rows(arr):
     return [int.from_bytes(r.tobytes(), "little") for r in arr]
 
 
-@pytest.mark.parametrize("name", ["k128", "k1024", "k2048"])
+@pytest.mark.parametrize("name", ["k128", "k1024", "k2048", "k3072"])
 def test_cpuref_matches_oracle(name):
     k = key_of(name)
     rng = random.Random(3)

@@ -22,8 +22,9 @@ from hebatch.backends import NaiveBackend  # noqa: E402
 from hebatch.batches import CiphertextBatch, PlaintextBatch, encode_batch  # noqa: E402
 from hebatch.paillier import default_rng, draw_unit, keygen, keypair_from_primes  # noqa: E402
 
-KEYS = {"tiny": None, "k128": (128, 1234), "k512": (512, 99), "k1024": (1024, 7), "k2048": (2048, 7)}
-COUNT = {"tiny": 6, "k128": 8, "k512": 6, "k1024": 5, "k2048": 4}
+KEYS = {"tiny": None, "k128": (128, 1234), "k512": (512, 99), "k1024": (1024, 7), "k2048": (2048, 7),
+        "k3072": (3072, 7)}
+COUNT = {"tiny": 6, "k128": 8, "k512": 6, "k1024": 5, "k2048": 4, "k3072": 3}
 
 
 def hx(v):

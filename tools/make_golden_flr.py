@@ -67,6 +67,8 @@ if __name__ == "__main__":
         "small_uncached": run(96, 6, 512, 16, 2, seed=5, key_seed=99, caching=False),
         "homo_1024": run_homo(1000, 8, 1024, 2, 3),
         "homo_8party_512": run_homo(400, 24, 512, 8, 2, seed=9, key_seed=99),
+        # BASELINE configs[3] shape (Paillier-2048, 200 features, full-batch steps) at 256 rows, two iterations
+        "full_batch_2048x200": run(256, 200, 2048, 256, 2),
     }}
     path = os.path.join(ROOT, "tests", "golden", "flr_config1.json")
     with open(path, "w") as fh:
