@@ -21,7 +21,12 @@ struct ModDev {
   uint32_t np;          // -n^-1 mod 2^32
 };
 // Resident 128-thread blocks per SM the kernels are compiled for (register budget 128 or 168).
-__host__ __device__ constexpr int blocks_per_sm(int lpt) { return lpt > 24 ? 2 : lpt > 20 ? 3 : lpt <= 8 ? 6 : 4; }
+#ifndef HB_NS_BLOCKS
+#define HB_NS_BLOCKS 2
+#endif
+__host__ __device__ constexpr int blocks_per_sm(int lpt) {
+  return lpt > 32 ? HB_NS_BLOCKS : lpt > 24 ? 2 : lpt > 20 ? 3 : lpt <= 8 ? 6 : 4;
+}
 template <int LPT>
 __device__ __forceinline__ void tile_store(uint32_t* tw, int e, const uint32_t (&x)[LPT]) {
   int lane = threadIdx.x & 31;
@@ -214,16 +219,25 @@ constexpr size_t sqr_smem_bytes() { return (size_t)hb::Mont<LPT, TPI>::SQ_WORDS 
 #define HB_DISPATCH_POW HB_DISPATCH
 #endif
 
-// k_encrypt: the nine shapes; (48, 4) takes its staging area as dynamic shared memory.
+// k_encrypt: the nine shapes; (48, 4) takes its operand staging area and the modulus copy as dynamic shared memory.
 #define HB_DISPATCH_ENC(cfg, KERNEL, launch, stream, args)                                              \
   if (launch.cfg == 8) {                                                                                \
     hb::KERNEL<48, 4><<<launch.blocks, launch.threads,                                                  \
-                        hb::Mont<48, 4>::STAGE_WORDS * hb::Mont<48, 4>::IPW * sizeof(uint32_t), stream>>>(args); \
+                        hb::Mont<48, 4>::NS_SMEM_WORDS * sizeof(uint32_t), stream>>>(args);               \
     hbi::g_launches++;                                                                                  \
   } else {                                                                                              \
     HB_DISPATCH_POW(cfg, KERNEL, launch, stream, args)                                                  \
   }
 
+#ifdef HB_DEV_ONLY_3072   /* development builds: only the shapes a 3072-bit key uses, for quick A/B experiments */
+#define HB_DISPATCH(cfg, KERNEL, launch, stream, args)                                           \
+  switch (launch.cfg) {                                                                                 \
+    case 2: hb::KERNEL<24, 4><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break; \
+    case 4: hb::KERNEL<24, 8><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break; \
+    default: return hbi::fail(HB_ERR_UNSUPPORTED, "no limb configuration");                            \
+  }                                                                                              \
+  hbi::g_launches++;
+#else
 #define HB_DISPATCH(cfg, KERNEL, launch, stream, args)                                           \
   switch (launch.cfg) {                                                                                 \
     case 0: hb::KERNEL<8, 4><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break;  \
@@ -237,5 +251,6 @@ constexpr size_t sqr_smem_bytes() { return (size_t)hb::Mont<LPT, TPI>::SQ_WORDS 
     default: return hbi::fail(HB_ERR_UNSUPPORTED, "no limb configuration");                            \
   }                                                                                              \
   hbi::g_launches++;
+#endif
 
 }  // namespace hbi

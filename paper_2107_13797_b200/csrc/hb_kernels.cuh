@@ -71,7 +71,7 @@ __device__ __forceinline__ void run_prog(const Mont<LPT, TPI>& mt, uint32_t (&x)
   }
 }
 
-extern __shared__ uint32_t hb_dyn_smem[];
+extern __shared__ __align__(16) uint32_t hb_dyn_smem[];
 // Shared-memory scratch of this lane's instance for Mont::sqr (nullptr when the shape has no dedicated squaring).
 template <int LPT, int TPI>
 __device__ __forceinline__ uint32_t* sqr_scratch() {
@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(32, 4 * blocks_per_sm(LPT)) k_encrypt(EncArgs 
   using M = Mont<LPT, TPI>;
   constexpr int IPW = 32 / TPI;
   M mt;
-  mt.init(A.mod.n, A.mod.np);
+  mt.init(A.mod.n, A.mod.np, hb_dyn_smem);
   // one warp per block: the tile loop then depends on blockIdx only, the compiler can see that the warp never
   // diverges, and every __shfl_sync becomes a bare SHFL instead of a WARPSYNC.COLLECTIVE / ENDCOLLECTIVE bracket
   const int lane = threadIdx.x, g = lane / TPI;
@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(32, 4 * blocks_per_sm(LPT)) k_fore_gradient(Fo
   using M = Mont<LPT, TPI>;
   constexpr int IPW = 32 / TPI;
   M mt;
-  mt.init(A.mod.n, A.mod.np);
+  mt.init(A.mod.n, A.mod.np, hb_dyn_smem);
   const int lane = threadIdx.x, g = lane / TPI;
   const long wg = blockIdx.x, nw = gridDim.x;
   uint32_t* tw = A.tbl + wg * A.tbl_stride;
@@ -490,7 +490,7 @@ __global__ void __launch_bounds__(32, 4 * blocks_per_sm(LPT)) k_decrypt(DecArgs 
       mt.neg_R(y);                                  // t = (u - 1) / s
       if (uzero) {
 #pragma unroll
-        for (int k = 0; k < LPT; k++) y[k] = mt.n[k];
+        mt.get_n(y);
         if (mt.t == 0) y[0] -= 1u;                  // s is odd: no borrow
       }
       mt.load_limbs(z, H.hsR);

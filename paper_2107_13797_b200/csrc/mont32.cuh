@@ -81,20 +81,107 @@ struct Mont {
   static constexpr int L = LPT * TPI;
   static constexpr uint32_t GM = TPI == 32 ? 0xffffffffu : ((1u << TPI) - 1u);
 
-  uint32_t n[LPT];     // modulus limbs owned by this lane
+  // NS ("modulus in shared memory") -- an experiment kept behind -DHB_NS_SHARED_MODULUS, OFF by default.  At LPT = 48
+  // (a 6144-bit modulus on four lanes) 48 limbs each of a and n next to 100 accumulator registers leave ptxas
+  // spilling ~3 KB per thread around the hot loop, so this variant keeps the modulus in shared memory, once per
+  // block (lane t's even limbs, then its odd limbs, at t * NS_STRIDE words: the four lanes' 16-byte reads fall on
+  // disjoint banks) and streams it back as LDS.128 a few multiplies ahead of use.  Measured on the B200 at
+  // 3072-bit keys (profiles/r02_shared_modulus_experiment.md): 28.3 k encrypt/s streamed (ld.volatile), 29.0 k
+  // when ptxas is allowed to cache the loads in registers again, against 29.9 k for the register-resident modulus
+  // with its spills -- the loads cost more issue slots than the spills they remove.  One warp per block.
+#ifdef HB_NS_SHARED_MODULUS
+  static constexpr bool NS = (LPT == 48);
+#else
+  static constexpr bool NS = false;
+#endif
+  static constexpr int NS_STRIDE = LPT + 4;
+  static constexpr int STAGE_WORDS = L + TPI;
+  static constexpr int NS_SMEM_WORDS = STAGE_WORDS * (32 / TPI) + TPI * NS_STRIDE;
+
+  uint32_t n[NS ? 1 : LPT];   // modulus limbs owned by this lane (register shapes)
   uint32_t np;         // -n^-1 mod 2^32
   int t;               // lane index inside the group
   int gshift;          // position of the group's lane 0 in the warp
   bool top;            // this lane holds the most significant limbs
+  uint32_t* ns_sa;     // NS: this instance's operand staging area (stride 32 / TPI)
+  uint32_t* ns_n;      // NS: this lane's modulus limbs in shared memory (H even limbs, then H odd limbs)
 
-  __device__ __forceinline__ void init(const uint32_t* __restrict__ n_limbs, uint32_t np_) {
+  // smem: NS shapes only -- NS_SMEM_WORDS words, 16-byte aligned, private to this warp
+  __device__ __forceinline__ void init(const uint32_t* __restrict__ n_limbs, uint32_t np_, uint32_t* smem = nullptr) {
     const int lane = threadIdx.x & 31;
     t = lane & (TPI - 1);
     gshift = lane & ~(TPI - 1);
     top = t == TPI - 1;
     np = np_;
+    if constexpr (NS) {
+      ns_sa = smem + lane / TPI;
+      ns_n = smem + STAGE_WORDS * (32 / TPI) + t * NS_STRIDE;
+      __syncwarp();
+      if (lane < TPI) {
 #pragma unroll
-    for (int i = 0; i < LPT; i++) n[i] = n_limbs[t * LPT + i];
+        for (int i = 0; i < LPT; i++) ns_n[(i >> 1) + (i & 1) * H] = n_limbs[t * LPT + i];
+      }
+      __syncwarp();
+    } else {
+#pragma unroll
+      for (int i = 0; i < LPT; i++) n[i] = n_limbs[t * LPT + i];
+    }
+  }
+  // the lane's modulus limbs as a register array (NS shapes: read from shared memory)
+  __device__ __forceinline__ void get_n(uint32_t (&v)[LPT]) const {
+#pragma unroll
+    for (int i = 0; i < LPT; i++) {
+      if constexpr (NS) v[i] = ns_n[(i >> 1) + (i & 1) * H];
+      else v[i] = n[i];
+    }
+  }
+  // E, O += n * x with the modulus streamed from shared memory: 16-byte reads, NS_PF chunks ahead of the multiplies
+#ifndef HB_NS_PF
+#define HB_NS_PF 3
+#endif
+#ifdef HB_NS_VOLATILE
+#define HB_NS_LD "ld.volatile.shared.v4.u32"
+#else
+#define HB_NS_LD "ld.shared.v4.u32"
+#endif
+  static constexpr int NS_PF = HB_NS_PF;
+  __device__ __forceinline__ void mac_row_ns(uint64_t (&E)[H + 1], uint64_t (&O)[H + 1], uint32_t x) const {
+    static_assert(!NS || H % 4 == 0, "shared-modulus rows read four limbs at a time");
+    constexpr int NCH = H / 2;                      // chunks of four limbs: H / 4 of evens, then H / 4 of odds
+    const uint32_t base = (uint32_t)__cvta_generic_to_shared(ns_n);
+    uint32_t c[NS_PF][4];
+#pragma unroll
+    for (int j = 0; j < NS_PF && j < NCH; j++)
+      asm volatile(HB_NS_LD " {%0, %1, %2, %3}, [%4];"
+                   : "=r"(c[j][0]), "=r"(c[j][1]), "=r"(c[j][2]), "=r"(c[j][3]) : "r"(base + 16u * j));
+#pragma unroll
+    for (int j = 0; j < NCH; j++) {
+      const uint32_t v0 = c[j % NS_PF][0], v1 = c[j % NS_PF][1], v2 = c[j % NS_PF][2], v3 = c[j % NS_PF][3];
+      if (j + NS_PF < NCH)
+        asm volatile(HB_NS_LD " {%0, %1, %2, %3}, [%4];"
+                     : "=r"(c[j % NS_PF][0]), "=r"(c[j % NS_PF][1]), "=r"(c[j % NS_PF][2]), "=r"(c[j % NS_PF][3])
+                     : "r"(base + 16u * (j + NS_PF)));
+      if (j < NCH / 2) {
+        const int i = 4 * j;
+        E[i] = j == 0 ? mac_cc(v0, x, E[i]) : macc_cc(v0, x, E[i]);
+        E[i + 1] = macc_cc(v1, x, E[i + 1]);
+        E[i + 2] = macc_cc(v2, x, E[i + 2]);
+        E[i + 3] = macc_cc(v3, x, E[i + 3]);
+        if (j == NCH / 2 - 1) E[H] = (uint64_t)addc32(lo32(E[H]), 0u);
+      } else {
+        const int i = 4 * (j - NCH / 2);
+        O[i] = j == NCH / 2 ? mac_cc(v0, x, O[i]) : macc_cc(v0, x, O[i]);
+        O[i + 1] = macc_cc(v1, x, O[i + 1]);
+        O[i + 2] = macc_cc(v2, x, O[i + 2]);
+        O[i + 3] = macc_cc(v3, x, O[i + 3]);
+        if (j == NCH - 1) O[H] = (uint64_t)addc32(lo32(O[H]), 0u);
+      }
+    }
+  }
+  // E, O += n * x
+  __device__ __forceinline__ void mac_row_n(uint64_t (&E)[H + 1], uint64_t (&O)[H + 1], uint32_t x) const {
+    if constexpr (NS) mac_row_ns(E, O, x);
+    else mac_row(E, O, n, x);
   }
 
   // E, O += v * x : one carry chain per accumulator array (H multiply-adds each)
@@ -154,8 +241,9 @@ struct Mont {
 
   // r in [0, 2n) given as limbs plus an overflow bit  ->  [0, n)
   __device__ __forceinline__ void cond_sub(uint32_t (&r)[LPT], uint32_t hi) const {
-    uint32_t d[LPT];
-    const uint32_t ge = sub_raw(d, r, n);
+    uint32_t d[LPT], nn[LPT];
+    get_n(nn);
+    const uint32_t ge = sub_raw(d, r, nn);
     if (hi | ge) {
 #pragma unroll
       for (int i = 0; i < LPT; i++) r[i] = d[i];
@@ -167,9 +255,10 @@ struct Mont {
     cond_sub(r, hi);
   }
   __device__ __forceinline__ void sub_mod(uint32_t (&r)[LPT], const uint32_t (&a)[LPT], const uint32_t (&b)[LPT]) const {
-    uint32_t d[LPT], s[LPT];
+    uint32_t d[LPT], s[LPT], nn[LPT];
     const uint32_t ge = sub_raw(d, a, b);
-    add_raw(s, d, n, 0u);               // unconditional: no warp collective inside a group-divergent branch
+    get_n(nn);
+    add_raw(s, d, nn, 0u);              // unconditional: no warp collective inside a group-divergent branch
 #pragma unroll
     for (int i = 0; i < LPT; i++) r[i] = ge ? d[i] : s[i];
   }
@@ -193,8 +282,12 @@ struct Mont {
   }
 
   __device__ __forceinline__ void mul(uint32_t (&r)[LPT], const uint32_t (&a)[LPT], const uint32_t (&b)[LPT]) const {
-    uint32_t unused[LPT];
-    mul_impl<false>(r, a, b, unused);
+    if constexpr (NS) {
+      mul_sf(r, a, b, ns_sa);
+    } else {
+      uint32_t unused[LPT];
+      mul_impl<false>(r, a, b, unused);
+    }
   }
   // mul() that also returns the Montgomery quotient Q = -(a*b) * n^-1 mod R (lane t gets its LPT limbs).
   // When a*b is a multiple of n:  a*b / n = (R - Q) mod R.
@@ -221,7 +314,7 @@ struct Mont {
         uint32_t q = (lo32(E[0]) + pend_lo) * np;
         q = __shfl_sync(FULLMASK, q, 0, TPI);
         if (COLLECT) { if (s == t) qd[i] = q; }
-        mac_row(E, O, n, q);
+        mac_row_n(E, O, q);
         // column 0 = E[0] + pend: its low word is zero on lane 0 and goes to the lane below elsewhere
         const uint32_t vlo = add_cc32(lo32(E[0]), pend_lo);
         const uint32_t vhi = addc_cc32(hi32(E[0]), pend_hi);
@@ -352,7 +445,7 @@ struct Mont {
         mac_row(E, O, a, bs[u * IPW]);
         uint32_t q = (lo32(E[0]) + pend_lo) * np;
         q = __shfl_sync(FULLMASK, q, 0, TPI);
-        mac_row(E, O, n, q);
+        mac_row_n(E, O, q);
         const uint32_t vlo = add_cc32(lo32(E[0]), pend_lo);
         const uint32_t vhi = addc_cc32(hi32(E[0]), pend_hi);
         const uint32_t vtop = addc32(0, 0);
@@ -368,7 +461,6 @@ struct Mont {
   // mul() with b read from shared memory and the rows of one lane block fully unrolled (no frame-rotation moves):
   // the form for LPT = 48, where a register copy of b would not fit next to the accumulators, a and n.
   // `sa`: this instance's staging area alone, STAGE_WORDS words at stride IPW.
-  static constexpr int STAGE_WORDS = L + TPI;
   __device__ __forceinline__ void mul_sf(uint32_t (&r)[LPT], const uint32_t (&a)[LPT], const uint32_t (&b)[LPT],
                                          uint32_t* sa) const {
     uint64_t E[H + 1], O[H + 1];
@@ -390,7 +482,7 @@ struct Mont {
         mac_row(E, O, a, bs[i * IPW]);
         uint32_t q = (lo32(E[0]) + pend_lo) * np;
         q = __shfl_sync(FULLMASK, q, 0, TPI);
-        mac_row(E, O, n, q);
+        mac_row_n(E, O, q);
         const uint32_t vlo = add_cc32(lo32(E[0]), pend_lo);
         const uint32_t vhi = addc_cc32(hi32(E[0]), pend_hi);
         const uint32_t vtop = addc32(0, 0);
@@ -529,7 +621,7 @@ struct Mont {
       for (int u = 0; u < RU; u++) {
         uint32_t q = (lo32(E[0]) + pend_lo) * np;
         q = __shfl_sync(FULLMASK, q, 0, TPI);
-        mac_row(E, O, n, q);
+        mac_row_n(E, O, q);
         const uint32_t vlo = add_cc32(lo32(E[0]), pend_lo);
         const uint32_t vhi = addc_cc32(hi32(E[0]), pend_hi);
         const uint32_t vtop = addc32(0, 0);
