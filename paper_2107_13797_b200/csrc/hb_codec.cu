@@ -177,21 +177,60 @@ __global__ void __launch_bounds__(64) k_decode_f64(CodecArgs A) {
 //
 // A residue is 4 * wn bytes of which, for every value a protocol ever encodes, all but three words are either zero
 // (positive) or the words of n (negative, n - |x|).  The thread-per-element kernels above spend hundreds of
-// instructions per element walking those words; the kernels below move the background with 16-byte accesses, 16
-// lanes per element, and leave only the three interesting words to one thread per element.  Requires wn % 4 == 0
-// and wn >= 8 (the host falls back to the kernels above otherwise).
+// instructions per element walking those words; the kernels below move the background with 32-byte accesses (whole
+// sectors), 8 lanes per element, and leave only the three interesting words to one thread per element.  Requires
+// wn % 8 == 0 and wn >= 8 (the host falls back to the kernels above otherwise).
 
-// encode: pass 1 stores the background (0 or n), pass 2 patches the up-to-three magnitude words and the borrow run
-template <bool TWO>     // TWO: more than 64 words per residue (a second 16-byte column per lane)
-__global__ void __launch_bounds__(256) k_encode_f64_wide(CodecArgs A) {
+// 32-byte global accesses (one full DRAM / L2 sector per lane): LDG.E.ENL2.256 / STG.E.ENL2.256 on sm_100a.
+__device__ __forceinline__ void ld8(uint32_t (&w)[8], const uint32_t* p) {
+  asm volatile("ld.global.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
+               : "l"(p));
+}
+__device__ __forceinline__ void st8(uint32_t* p, const uint32_t (&w)[8]) {
+  asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};"
+               :: "l"(p), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+               : "memory");
+}
+__device__ __forceinline__ void ldn8(uint32_t (&w)[8], const uint32_t* p) {      // constants: cached loads
+  const uint4 a = ld4(p), b = ld4(p + 4);
+  w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w; w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+}
+
+// encode: one lane per element works out the up-to-three magnitude words; the background (0 or n) of 32 elements
+// then goes out as 32-byte stores -- whole sectors, 8 lanes per element, four elements per warp instruction.  When
+// the warp's 32 elements agree on the sector their magnitude words fall into and none has a borrow running past
+// them -- every batch a protocol encodes -- that sector is left out of the background pass and written once,
+// patched, by the element's own lane: every sector is written exactly once and whole (a first cut that wrote the
+// patched 16 bytes separately from the other half of their sector ran at HALF the speed: partial-sector writes
+// make the L2 fetch the sector first).  Otherwise: background everywhere, __syncwarp, then word-sized patches.
+// The next batch's doubles are fetched before this batch's stores.  Requires wn % 8 == 0.
+#ifndef HB_ENC_BLOCKS
+#define HB_ENC_BLOCKS 4      // 62 registers, no spills; 5 and 6 blocks (48 / 40 registers) measured slower
+#endif
+template <bool TWO>     // TWO: more than 64 words per residue (a second 32-byte column per lane)
+__global__ void __launch_bounds__(256, HB_ENC_BLOCKS) k_encode_f64_wide(CodecArgs A) {
   const int lane = threadIdx.x & 31;
   const long warp = (long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const long nwarps = (long)gridDim.x * (blockDim.x >> 5);
   const int wn = A.wn, T = A.maxint_top;
-  for (long eb = warp * 32; eb < A.count; eb += nwarps * 32) {
+  const int quarter = lane >> 3, l8 = lane & 7, i0 = 8 * l8;
+  const bool act0 = i0 < wn, act1 = TWO && i0 + 64 < wn;
+  uint32_t nv0[8], nv1[8];
+#pragma unroll
+  for (int k = 0; k < 8; k++) { nv0[k] = 0u; nv1[k] = 0u; }
+  if (act0) ldn8(nv0, A.nwords + i0);
+  if (act1) ldn8(nv1, A.nwords + i0 + 64);
+  long eb = warp * 32;
+  unsigned long long bits_next = eb + lane < A.count ? (unsigned long long)__double_as_longlong(A.fin[eb + lane]) : 0ull;
+  for (; eb < A.count; eb += nwarps * 32) {
     const long e = eb + lane;
     const bool have = e < A.count;
-    const unsigned long long bits = have ? (unsigned long long)__double_as_longlong(A.fin[e]) : 0ull;
+    const unsigned long long bits = bits_next;
+    {
+      const long en = e + nwarps * 32;
+      bits_next = en < A.count ? (unsigned long long)__double_as_longlong(A.fin[en]) : 0ull;
+    }
     const bool negv = (bits >> 63) != 0;
     const int e11 = (int)((bits >> 52) & 0x7ff);
     unsigned long long mant = bits & 0xfffffffffffffull;
@@ -202,8 +241,8 @@ __global__ void __launch_bounds__(256) k_encode_f64_wide(CodecArgs A) {
       long s = -shift;
       if (s >= 64) mant = 0;
       else {
-        unsigned long long q = mant >> s, rem = mant & ((1ull << s) - 1ull), half = 1ull << (s - 1);
-        if (rem > half || (rem == half && (q & 1ull))) q++;
+        unsigned long long q = mant >> s, rem = mant & ((1ull << s) - 1ull), half_ulp = 1ull << (s - 1);
+        if (rem > half_ulp || (rem == half_ulp && (q & 1ull))) q++;
         mant = q;
       }
       shift = 0;
@@ -244,99 +283,152 @@ __global__ void __launch_bounds__(256) k_encode_f64_wide(CodecArgs A) {
         while (bend < wn && A.nwords[bend] == 0u) bend++;
       }
     }
-    // pass 1: background, two elements per step, 16 lanes x 16 bytes each
     const uint32_t negmask = __ballot_sync(0xffffffffu, neg);
-    {
-      const int half = lane >> 4, i0 = 4 * (lane & 15);
-      const bool act0 = i0 < wn, act1 = TWO && i0 + 64 < wn;
-      const uint4 zero4 = make_uint4(0u, 0u, 0u, 0u);
-      const uint4 nv0 = act0 ? ld4(A.nwords + i0) : zero4, nv1 = act1 ? ld4(A.nwords + i0 + 64) : zero4;
-      const bool full = eb + 32 <= A.count;
-      uint32_t* q = A.mout + (eb + half) * (long)wn + i0;
+    const bool full = eb + 32 <= A.count;
+    uint32_t* q = A.mout + (eb + quarter) * (long)wn + i0;
+    // do the 32 elements agree on the sector of their magnitude words, with nothing running past it?
+    const int sw = over ? 0 : (int)(ws >> 3);
+    const int sw0 = __shfl_sync(0xffffffffu, sw, 0);
+    const bool plain = !have || over || (sw == sw0 && !brun && (ws & 7) <= 5);
+    const bool fast = __all_sync(0xffffffffu, plain);
+    // pass 1: background, four elements per step (the shared sector left out on the fast path)
+    const bool put0 = act0 && !(fast && l8 == sw0), put1 = TWO && act1 && !(fast && l8 + 8 == sw0);
 #pragma unroll
-      for (int s = 0; s < 32; s += 2) {
-        const bool in = full || eb + s + half < A.count;
-        const bool isneg = (negmask >> (s + half)) & 1u;
-        if (act0 && in) *reinterpret_cast<uint4*>(q + (long)s * wn) = isneg ? nv0 : zero4;
-        if (TWO && act1 && in) *reinterpret_cast<uint4*>(q + (long)s * wn + 64) = isneg ? nv1 : zero4;
+    for (int s = 0; s < 32; s += 4) {
+      const bool in = full || eb + s + quarter < A.count;
+      const uint32_t keep = ((negmask >> (s + quarter)) & 1u) ? 0xffffffffu : 0u;
+      if (put0 && in) {
+        uint32_t w[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++) w[k] = nv0[k] & keep;
+        st8(q + (long)s * wn, w);
+      }
+      if (put1 && in) {
+        uint32_t w[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++) w[k] = nv1[k] & keep;
+        st8(q + (long)s * wn + 64, w);
       }
     }
-    __syncwarp();
-    // pass 2: the words that differ from the background
-    if (have && !over) {
-      uint32_t* dst = A.mout + e * wn;
-      if (ws < wn) dst[ws] = v0;
-      if (ws + 1 < wn) dst[ws + 1] = v1;
-      if (ws + 2 < wn) dst[ws + 2] = v2;
-      if (brun) {
-        for (long i = ws + 3; i < bend; i++) dst[i] = 0xffffffffu;
-        if (bend < wn) dst[bend] = A.nwords[bend] - 1u;
+    if (fast) {
+      // pass 2: the element's own lane writes that sector, magnitude words in place
+      if (have) {
+        uint32_t c[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++) c[k] = 0u;
+        if (neg) ldn8(c, A.nwords + 8 * sw0);
+        if (!over) {
+          const int pos = (int)(ws & 7);
+#pragma unroll
+          for (int k = 0; k < 8; k++) c[k] = k == pos ? v0 : k == pos + 1 ? v1 : k == pos + 2 ? v2 : c[k];
+        }
+        st8(A.mout + e * (long)wn + 8 * sw0, c);
       }
+    } else {
+      __syncwarp();
+      // pass 2: the words that differ from the background
+      if (have && !over) {
+        uint32_t* dst = A.mout + e * (long)wn;
+        if (ws < wn) dst[ws] = v0;
+        if (ws + 1 < wn) dst[ws + 1] = v1;
+        if (ws + 2 < wn) dst[ws + 2] = v2;
+        if (brun) {
+          for (long i = ws + 3; i < bend; i++) dst[i] = 0xffffffffu;
+          if (bend < wn) dst[bend] = A.nwords[bend] - 1u;
+        }
+      }
+      __syncwarp();
     }
-    __syncwarp();
   }
 }
 
 // decode: pass 1 checks that every word from the fourth up is background (all zero, or all equal to n); pass 2
 // turns the low 96 bits into the correctly rounded double.  Anything else -- wide magnitudes, the overflow band --
 // is marked in A.slow for the generic kernel.  Needs max_int >= 2^96 (maxint_top >= 3).
+#ifndef HB_DEC_BLOCKS
+#define HB_DEC_BLOCKS 4      // 64 registers; measured 0.917 of the HBM copy peak with two steps in flight, 0.89 with
+#endif                       // four (62 registers + spills), 0.66 at 5 blocks (48 registers, spills)
+#ifndef HB_DEC_NJ
+#define HB_DEC_NJ 2
+#endif
 template <bool TWO>
-__global__ void __launch_bounds__(256, 4) k_decode_f64_wide(CodecArgs A) {
+__global__ void __launch_bounds__(256, HB_DEC_BLOCKS) k_decode_f64_wide(CodecArgs A) {
   const int lane = threadIdx.x & 31;
   const long warp = (long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const long nwarps = (long)gridDim.x * (blockDim.x >> 5);
   const int wn = A.wn;
-  const int half = lane >> 4, l16 = lane & 15, i0 = 4 * l16;
-  const bool act0 = i0 < wn, act1 = TWO && i0 + 64 < wn;
-  const uint4 zero4 = make_uint4(0u, 0u, 0u, 0u);
-  const uint4 nv0 = act0 ? ld4(A.nwords + i0) : zero4, nv1 = act1 ? ld4(A.nwords + i0 + 64) : zero4;
-  const uint32_t low3 = l16 ? 0xffffffffu : 0u;          // lane 0 of an element ignores its words 0..2
-  for (long eb = warp * 32; eb < A.count; eb += nwarps * 32) {
-    // own element's low words first: their latency hides behind pass 1
-    const long e = eb + lane;
-    uint32_t m0 = 0, m1 = 0, m2 = 0;
-    if (e < A.count) {
-      const uint32_t* x = A.min + e * wn;
-      m0 = x[0]; m1 = x[1]; m2 = x[2];
-    }
-    const bool full = eb + 32 <= A.count;
-    const uint32_t* p = A.min + (eb + half) * (long)wn + i0;
-    uint32_t zbits = 0, nbits = 0;        // bit k: every word from the fourth up of element eb + k is 0 / equals n
-#pragma unroll 1
-    for (int s = 0; s < 32; s += 8) {     // four steps of two elements, loads issued together
-      uint4 xa[4], xb[4];
+  const int quarter = lane >> 3, l8 = lane & 7, i0 = 8 * l8;
+  // sector 0 (words 0..7) of an element is read by the element's own lane, not in pass 1
+  const bool act0 = i0 < wn && l8 != 0, act1 = TWO && i0 + 64 < wn;
+  uint32_t nv0[8], nv1[8], nlow[8];
 #pragma unroll
-      for (int j = 0; j < 4; j++) {
-        const bool in = full || eb + s + 2 * j + half < A.count;
-        xa[j] = (act0 && in) ? ld4(p + (long)(s + 2 * j) * wn) : nv0;
-        xb[j] = (TWO && act1 && in) ? ld4(p + (long)(s + 2 * j) * wn + 64) : nv1;
+  for (int k = 0; k < 8; k++) { nv0[k] = 0u; nv1[k] = 0u; }
+  if (act0) ldn8(nv0, A.nwords + i0);
+  if (act1) ldn8(nv1, A.nwords + i0 + 64);
+  ldn8(nlow, A.nwords);
+  constexpr int NJ = TWO ? (HB_DEC_NJ > 1 ? HB_DEC_NJ / 2 : 1) : HB_DEC_NJ;   // steps of four elements in flight
+  for (long eb = warp * 32; eb < A.count; eb += nwarps * 32) {
+    // own element's low sector first: its latency hides behind pass 1
+    const long e = eb + lane;
+    uint32_t m[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) m[k] = 0u;
+    if (e < A.count) ld8(m, A.min + e * (long)wn);
+    uint32_t m0 = m[0], m1 = m[1], m2 = m[2];
+    const bool full = eb + 32 <= A.count;
+    const uint32_t* p = A.min + (eb + quarter) * (long)wn + i0;
+    uint32_t zbits = 0, nbits = 0;        // bit k: every word from the ninth up of element eb + k is 0 / equals n
+#pragma unroll 1
+    for (int s = 0; s < 32; s += 4 * NJ) {     // loads of NJ steps issued together
+      uint32_t xa[NJ][8], xb[TWO ? NJ : 1][8];
+#pragma unroll
+      for (int j = 0; j < NJ; j++) {
+        const bool in = full || eb + s + 4 * j + quarter < A.count;
+        if (act0 && in) ld8(xa[j], p + (long)(s + 4 * j) * wn);
+        else {
+#pragma unroll
+          for (int k = 0; k < 8; k++) xa[j][k] = nv0[k];
+        }
+        if (TWO) {
+          if (act1 && in) ld8(xb[j], p + (long)(s + 4 * j) * wn + 64);
+          else {
+#pragma unroll
+            for (int k = 0; k < 8; k++) xb[j][k] = nv1[k];
+          }
+        }
       }
 #pragma unroll
-      for (int j = 0; j < 4; j++) {
-        uint32_t z = ((xa[j].x | xa[j].y | xa[j].z) & low3) | xa[j].w;
-        uint32_t d = (((xa[j].x ^ nv0.x) | (xa[j].y ^ nv0.y) | (xa[j].z ^ nv0.z)) & low3) | (xa[j].w ^ nv0.w);
+      for (int j = 0; j < NJ; j++) {
+        uint32_t z = 0u, d = 0u;
+#pragma unroll
+        for (int k = 0; k < 8; k++) { z |= xa[j][k]; d |= xa[j][k] ^ nv0[k]; }
         if (TWO) {
-          z |= xb[j].x | xb[j].y | xb[j].z | xb[j].w;
-          d |= (xb[j].x ^ nv1.x) | (xb[j].y ^ nv1.y) | (xb[j].z ^ nv1.z) | (xb[j].w ^ nv1.w);
+#pragma unroll
+          for (int k = 0; k < 8; k++) { z |= xb[j][k]; d |= xb[j][k] ^ nv1[k]; }
         }
         // inactive lanes hold n's (zero) words: they vote "equal to n" and, being zero, "zero" as well
         const uint32_t bz = __ballot_sync(0xffffffffu, z == 0u), bn = __ballot_sync(0xffffffffu, d == 0u);
-        const int first = s + 2 * j;
-        zbits |= ((uint32_t)((bz & 0xffffu) == 0xffffu) << first) | ((uint32_t)((bz >> 16) == 0xffffu) << (first + 1));
-        nbits |= ((uint32_t)((bn & 0xffffu) == 0xffffu) << first) | ((uint32_t)((bn >> 16) == 0xffffu) << (first + 1));
+        const int first = s + 4 * j;
+#pragma unroll
+        for (int qq = 0; qq < 4; qq++) {
+          zbits |= (uint32_t)(((bz >> (8 * qq)) & 0xffu) == 0xffu) << (first + qq);
+          nbits |= (uint32_t)(((bn >> (8 * qq)) & 0xffu) == 0xffu) << (first + qq);
+        }
       }
     }
-    const bool my_zero = (zbits >> lane) & 1u, my_n = (nbits >> lane) & 1u;
+    const uint32_t hz = m[3] | m[4] | m[5] | m[6] | m[7];
+    const uint32_t hn = (m[3] ^ nlow[3]) | (m[4] ^ nlow[4]) | (m[5] ^ nlow[5]) | (m[6] ^ nlow[6]) | (m[7] ^ nlow[7]);
+    const bool my_zero = ((zbits >> lane) & 1u) && hz == 0u, my_n = ((nbits >> lane) & 1u) && hn == 0u;
     if (e >= A.count) continue;
     bool neg = false, slow = false;
     if (my_zero) {
       // positive, below 2^96 <= max_int
     } else if (my_n) {
-      unsigned long long d = (unsigned long long)A.nwords[0] - m0;
+      unsigned long long d = (unsigned long long)nlow[0] - m0;
       m0 = (uint32_t)d;
-      d = (unsigned long long)A.nwords[1] - m1 - (d >> 63);
+      d = (unsigned long long)nlow[1] - m1 - (d >> 63);
       m1 = (uint32_t)d;
-      d = (unsigned long long)A.nwords[2] - m2 - (d >> 63);
+      d = (unsigned long long)nlow[2] - m2 - (d >> 63);
       m2 = (uint32_t)d;
       neg = true;
       slow = (d >> 63) != 0 || (m0 | m1 | m2) == 0u;     // x >= n: not a residue; let the generic path judge it
@@ -467,6 +559,18 @@ __global__ void __launch_bounds__(64) k_plain_rescale(CodecArgs A) {
 
 }  // namespace hb
 
+namespace {
+// 256-thread blocks of `kernel` resident per SM on the current device (occupancy API; a handful of microseconds).
+int resident_blocks(const void* kernel) {
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kernel, 256, 0) != cudaSuccess || nb < 1) {
+    cudaGetLastError();
+    nb = 4;
+  }
+  return nb;
+}
+}  // namespace
+
 extern "C" {
 
 int hb_min_exact_exponent(hb_ctx* ctx, const double* values, int64_t count, int* min_out, void* stream_) {
@@ -510,10 +614,13 @@ int hb_encode_f64(hb_ctx* ctx, const double* values, int exponent, uint32_t* m_o
   A.negband = ctx->d_pub + ctx->off_negband; A.wn = ctx->wn; A.exponent = exponent; A.count = count;
   A.fin = values; A.mout = m_out; A.first_bad = (unsigned long long*)first_bad;
   A.maxint_top = ctx->maxint_top;
-  if (ctx->wn % 4 == 0 && ctx->wn >= 8 && ctx->wn <= 128) {
+  if (ctx->wn % 8 == 0 && ctx->wn >= 8 && ctx->wn <= 128) {
+    // persistent grid: exactly the blocks that are resident at once (no partial wave), grid-stride over batches of 32
     const long warps = (count + 31) / 32;
-    const long blocks = std::min<long>((warps + 7) / 8, (long)ctx->sms * 8);
-    if (ctx->wn > 64) hb::k_encode_f64_wide<true><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream_>>>(A);
+    const bool two = ctx->wn > 64;
+    const long blocks = std::min<long>((warps + 7) / 8, (long)ctx->sms * resident_blocks(two ? (const void*)hb::k_encode_f64_wide<true>
+                                                                                             : (const void*)hb::k_encode_f64_wide<false>));
+    if (two) hb::k_encode_f64_wide<true><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream_>>>(A);
     else hb::k_encode_f64_wide<false><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream_>>>(A);
   } else {
     const int threads = 64;
@@ -538,7 +645,7 @@ int hb_decode_f64(hb_ctx* ctx, const uint32_t* m, int exponent, double* values_o
   A.maxint_top = ctx->maxint_top;
   cudaStream_t stream = (cudaStream_t)stream_;
   uint8_t* scratch = nullptr;
-  if (ctx->wn % 4 == 0 && ctx->wn >= 8 && ctx->wn <= 128 && ctx->maxint_top >= 3) {
+  if (ctx->wn % 8 == 0 && ctx->wn >= 8 && ctx->wn <= 128 && ctx->maxint_top >= 3) {
     // marks of the elements left to the generic kernel: per call, from the library's pool (calls on one context
     // may run on several streams / threads at once)
     CU(hbi::pool_alloc(ctx->pool, (void**)&scratch, (size_t)count + 16, stream));
@@ -547,8 +654,10 @@ int hb_decode_f64(hb_ctx* ctx, const uint32_t* m, int exponent, double* values_o
     A.nslow = (unsigned long long*)scratch;
     CU(cudaMemsetAsync(scratch, 0, 8, stream));
     const long warps = (count + 31) / 32;
-    const long blocks = std::min<long>((warps + 7) / 8, (long)ctx->sms * 4);
-    if (ctx->wn > 64) hb::k_decode_f64_wide<true><<<(unsigned)blocks, 256, 0, stream>>>(A);
+    const bool two = ctx->wn > 64;
+    const long blocks = std::min<long>((warps + 7) / 8, (long)ctx->sms * resident_blocks(two ? (const void*)hb::k_decode_f64_wide<true>
+                                                                                             : (const void*)hb::k_decode_f64_wide<false>));
+    if (two) hb::k_decode_f64_wide<true><<<(unsigned)blocks, 256, 0, stream>>>(A);
     else hb::k_decode_f64_wide<false><<<(unsigned)blocks, 256, 0, stream>>>(A);
     g_launches++;
     A.only = slow;

@@ -164,6 +164,11 @@ class WordArray:
                 self._dev = host.cuda(non_blocking=False)
         return self._dev
 
+    def make_resident(self) -> None:
+        """Have the array in HBM in a form the kernels read (Arena.upload / restore after a spill)."""
+        if self.count and not self.on_device:
+            self.device()
+
     def ptr(self) -> int:
         return self.device().data_ptr() if self.count else 0
 
@@ -348,6 +353,12 @@ class CompactScalars(WordArray):
     @property
     def on_device(self) -> bool:
         return self.mag is not None
+
+    def make_resident(self) -> None:
+        """The compact form IS the resident form: nothing to upload while it is there (materialising 256-byte
+        residues for a 1M x 101 feature block would be 26 GB and minutes of host work)."""
+        if not self.on_device:
+            super().make_resident()
 
     def numpy(self) -> np.ndarray:
         if self._np is None:
