@@ -263,14 +263,19 @@ int matvec_ab(hb_ctx* ctx, const uint32_t* cm, const PrepOut& pr, long colstride
   const int L = Ldig(cfg);
   hb::ModDev mod = dev_mod(ctx->d_pub, ctx->mod_n2);
   // Window width by row count.  Per column and window the bucket work is about 6 * 2^c multiplications next to one
-  // per row: 9 bits (one window fewer than 8 for 52-bit scalars) pays from 32 k rows, 13 bits (four windows instead
-  // of six) from 200 k rows (measured break-even ~150 k) -- there the fold over the 8192 digit values runs in parallel pieces.
-  int cbits = inner >= 200000 ? 13 : inner >= 32768 ? 9
+  // per row, so wider windows pay once the rows outnumber the buckets: measured for 52-bit scalars, d = 100
+  // (profiles/r02_matvec_window_sweep.json) -- 9 bits from 32 k rows; 11 bits (five windows instead of six) from
+  // 64 k rows (100 k x 100: 246 ms against 266 ms); 13 bits (four windows) from 200 k rows (1 M x 100: 1.79 s
+  // against 2.11 s at 11 bits, 2.50 s at 9) -- from 11 bits up the fold over the digit values runs in parallel pieces.
+  int cbits = inner >= 200000 ? 13 : inner >= 65536 ? 11 : inner >= 32768 ? 9
             : inner >= 4096 ? 8 : inner >= 1024 ? 7 : inner >= 256 ? 6 : inner >= 64 ? 5 : inner >= 16 ? 3 : 2;
   const bool forced = ctx->opt_matvec_cbits != 0;             // hb_ctx_set_option(HB_OPT_MATVEC_WINDOW_BITS)
   if (forced) cbits = ctx->opt_matvec_cbits;
-  if (cbits == 13 && (std::max(pr.maxbits, 1) + 12) / 13 >= (std::max(pr.maxbits, 1) + 8) / 9 && !forced)
-    cbits = 9;                                                 // no window saved: stay with the cheaper buckets
+  if (!forced) {                                               // no window saved: stay with the cheaper buckets
+    const int mb = std::max(pr.maxbits, 1);
+    if (cbits == 13 && (mb + 12) / 13 >= (mb + 10) / 11) cbits = 11;
+    if (cbits == 11 && (mb + 10) / 11 >= (mb + 8) / 9) cbits = 9;
+  }
   const int maxbits = std::max(pr.maxbits, 1);
   const int nwin = (maxbits + cbits - 1) / cbits;
   const int NB = 2 << cbits;
