@@ -62,6 +62,9 @@ def parse_args():
     ap.add_argument("--flr-rows", type=int, default=50_000,
                     help="rows of the heterogeneous-FLR extra (BASELINE configs[3] shape, 200 features)")
     ap.add_argument("--flr-iters", type=int, default=2, help="FLR iterations (the last one is reported)")
+    ap.add_argument("--flr-devices", default="",
+                    help="CUDA device indices of the FLR extra's multi-device backend (default: one per rank of "
+                         "--gpus; an index may repeat, e.g. 0,0 exercises the sharded path on one GPU)")
     ap.add_argument("--flr-cpu-rows", type=int, default=512,
                     help="rows of the same FLR iteration timed on the host CPU (0 = skip)")
     ap.add_argument("--check", type=int, default=4096, help="strided elements compared with the CPU oracle")
@@ -532,7 +535,8 @@ def run_b200(args):
     if not args.no_flr and count >= 100_000:
         if world > 1:
             time.sleep(2.0)                      # the other ranks are leaving their GPUs
-        extras.update(flr_extra(args.flr_rows, world, args.flr_iters))
+        devices = [int(v) for v in args.flr_devices.split(",")] if args.flr_devices else list(range(world))
+        extras.update(flr_extra(args.flr_rows, devices, args.flr_iters))
         if args.flr_cpu_rows > 0:
             extras.update(flr_cpu_extra(args.flr_cpu_rows, extras["flr_hetero_iter_s"], args.flr_rows))
 
@@ -579,11 +583,11 @@ def run_b200(args):
     print(json.dumps(line), flush=True)
 
 
-def flr_extra(rows: int, n_devices: int = 1, iters: int = 2, features: int = 200):
+def flr_extra(rows: int, devices=(0,), iters: int = 2, features: int = 200):
     """Full-batch iterations (gradient step + loss over all rows) of 2-party heterogeneous FLR through the
     package's operator API at Paillier-2048; the last one is reported (the first also encodes the feature
     matrices, which stay resident).  Per iteration: 5 * rows full-width modular powers, two rows x ~100 encrypted
-    matvecs, ~3 * rows scalar powers, ~4 * rows modular products, 202 decryptions.  With n_devices > 1 the
+    matvecs, ~3 * rows scalar powers, ~4 * rows modular products, 202 decryptions.  With more than one device the
     operators run on the single-process multi-device backend (element shards per device, matvec partials
     combined on the first device)."""
     import numpy as np
@@ -593,16 +597,17 @@ def flr_extra(rows: int, n_devices: int = 1, iters: int = 2, features: int = 200
     ids, X, y = flr.make_synthetic(rows, features, seed=42)
     guest, host = flr.vertical_split(ids, X, y, 2)
     keys = paillier.keygen(KEY_BITS, paillier.default_rng(KEY_SEED), allow_insecure=True)
-    backend = MultiDeviceBackend(list(range(n_devices))) if n_devices > 1 else None
+    devices = list(devices)
+    backend = MultiDeviceBackend(devices) if len(devices) > 1 else None
     fed = flr.HeteroFederation(guest, host, [np.arange(rows)], np.arange(rows), keys,
                                flr.FlrConfig(0.15, rows, seed=42), backend=backend)
     secs, losses = [], []
     for _ in range(max(2, iters)):
-        for dev in range(n_devices):
+        for dev in set(devices):
             torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
         res = fed.run_epoch()
-        for dev in range(n_devices):
+        for dev in set(devices):
             torch.cuda.synchronize(dev)
         secs.append(time.perf_counter() - t0)
         losses.append(res.loss)
@@ -611,7 +616,7 @@ def flr_extra(rows: int, n_devices: int = 1, iters: int = 2, features: int = 200
     if backend is not None:
         backend.close()
     return {"flr_hetero_iter_s": secs[-1], "flr_first_iter_s": secs[0], "flr_iter_s_all": secs, "flr_rows": rows,
-            "flr_features": features, "flr_devices": n_devices,
+            "flr_features": features, "flr_devices": len(devices), "flr_device_ids": devices,
             "flr_modexp_per_iter": 5 * rows + 2 * (features + 1) + 1, "flr_loss": losses}
 
 

@@ -1,6 +1,7 @@
 """Condense `ncu --set full` reports into the JSON kept under profiles/.
 
     python tools/ncu_summary.py OUT.json name=report.ncu-rep [name=report.ncu-rep ...]
+    python tools/ncu_summary.py OUT.json name=report.raw.csv ...      (the `ncu -i rep --page raw --csv` export)
 
 For every report the first captured kernel's headline metrics are kept: duration, launch shape, registers,
 pipe utilisation (the integer multiplier lives on the "fmaheavy" pipe), issue activity, warp-stall mix,
@@ -41,8 +42,12 @@ KEEP = [
 
 
 def summarise(report: str) -> dict:
-    raw = subprocess.run(["ncu", "-i", report, "--page", "raw", "--csv"], capture_output=True, text=True, check=True)
-    rows = list(csv.reader(io.StringIO(raw.stdout)))
+    if report.endswith(".csv"):
+        text = open(report).read()
+    else:
+        text = subprocess.run(["ncu", "-i", report, "--page", "raw", "--csv"], capture_output=True, text=True,
+                              check=True).stdout
+    rows = [r for r in csv.reader(io.StringIO(text)) if len(r) > 10]
     head, units, first = rows[0], rows[1], rows[2]
     out = {}
     for h, u, v in zip(head, units, first):
