@@ -144,6 +144,16 @@ class HeteroFederation:
         return self.arena.ledger
 
     # ---- building blocks -----------------------------------------------------------------------------
+    @staticmethod
+    def _take(X, idx):
+        """X[idx] -- without the copy when idx selects every row in order (full-batch steps: 800 MB per call at
+        1M x 100, four calls per iteration)."""
+        idx = np.asarray(idx)
+        n = X.shape[0]
+        if idx.shape == (n,) and n and idx[0] == 0 and idx[-1] == n - 1 and bool((np.diff(idx) == 1).all()):
+            return X
+        return X[idx]
+
     def _mask_and_ship(self, grad_cipher, rng: random.Random):
         """Additive mask on the codec grid, re-randomise, serialise (parties.py:122-132)."""
         pk, be = self.pk, self.backend
@@ -167,7 +177,7 @@ class HeteroFederation:
         instead of a 256-byte residue -- which is what the encrypted matvec reads."""
         hit = cache.get(batch_id)
         if hit is None:
-            hit = cache[batch_id] = encode_batch(self.pk, X[idx], backend=self.backend, compact=True)
+            hit = cache[batch_id] = encode_batch(self.pk, self._take(X, idx), backend=self.backend, compact=True)
         return hit
 
     # ---- one mini-batch (parties.py:330-340) -------------------------------------------------------------
@@ -175,14 +185,14 @@ class HeteroFederation:
         pk, be = self.pk, self.backend
         s = len(idx)
         # host -> guest: encrypted logits
-        logits_h = self.host_X[idx] @ self.host_theta
+        logits_h = self._take(self.host_X, idx) @ self.host_theta
         wire = serialize_to_bytes(operators.batch_encrypt(
             pk, _encode(pk, logits_h, protocol_exponent(logits_h, pk=pk, backend=be), be), self.host_rng, be))
         # guest: fore gradient through the arena pipeline, then its gradient slice
         c_lh = deserialize(wire, pk)
         exponent = c_lh.exponents[0]
-        lg_plain = _encode(pk, self.guest_X[idx] @ self.guest_theta, exponent, be)
-        label_plain = _encode(pk, self.guest_y[idx], 0, be)
+        lg_plain = _encode(pk, self._take(self.guest_X, idx) @ self.guest_theta, exponent, be)
+        label_plain = _encode(pk, self._take(self.guest_y, idx), 0, be)
         if self.arena.caching_enabled:
             h_lh = self.arena.upload(c_lh)
             h_fore = self.arena.run_fore_gradient_pipeline(h_lh, lg_plain, label_plain)
@@ -215,15 +225,15 @@ class HeteroFederation:
     def loss(self) -> float:
         pk, be = self.pk, self.backend
         idx = self.loss_indices
-        z_h = self.host_X[idx] @ self.host_theta
+        z_h = self._take(self.host_X, idx) @ self.host_theta
         sq = z_h * z_h
         c1 = operators.batch_encrypt(pk, _encode(pk, z_h, protocol_exponent(z_h, pk=pk, backend=be), be),
                                      self.host_rng, be)
         c2 = operators.batch_encrypt(pk, _encode(pk, sq, protocol_exponent(sq, pk=pk, backend=be), be),
                                      self.host_rng, be)
         c_lh, c_lh2 = deserialize(serialize_to_bytes(c1), pk), deserialize(serialize_to_bytes(c2), pk)
-        lg = self.guest_X[idx] @ self.guest_theta
-        y = self.guest_y[idx]
+        lg = self._take(self.guest_X, idx) @ self.guest_theta
+        y = self._take(self.guest_y, idx)
         k1 = 0.25 * lg - 0.5 * y
         plain_part = LOG2 - 0.5 * y * lg + 0.125 * lg * lg
         e1, e2 = c_lh.exponents[0], c_lh2.exponents[0]
