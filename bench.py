@@ -57,6 +57,8 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-flr", action="store_true")
     ap.add_argument("--no-ops", action="store_true", help="skip the per-operator rates in extras")
+    ap.add_argument("--e2e-max-steps", type=int, default=10,
+                    help="the host-buffer end-to-end leg times min(--steps, this) steps of 2M operations each")
     ap.add_argument("--no-api", action="store_true", help="skip the operator-API end-to-end leg")
     ap.add_argument("--api-steps", type=int, default=5, help="timed steps of the operator-API end-to-end leg")
     ap.add_argument("--flr-rows", type=int, default=50_000,
@@ -365,7 +367,7 @@ def run_b200(args):
 
         host_step()
         barrier()
-        e2e_steps = max(1, args.steps)
+        e2e_steps = max(1, min(args.steps, args.e2e_max_steps))      # bounded so that a --steps 20 run stays within minutes
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
             host_step()

@@ -59,3 +59,24 @@ def test_homo_flr_equals_reference(name):
     assert [r.grad_norm.hex() for r in results] == case["grad_norm"]
     assert [float(v).hex() for v in fed.theta] == case["theta"]
     assert [[float(v).hex() for v in g] for g in fed.aggregated_gradients] == case["aggregated_gradients"]
+
+
+def test_full_batch_iteration_equals_cpu_oracle_iteration():
+    """The check bench.py makes beside its FLR timing, as a test: full-batch iterations (idx = every row in order, the
+    path that skips the row gather) on the GPU against oracle/flr_cpu.py (GMP) with the same data, key and seeds --
+    every decrypted masked gradient and the loss equal, float for float."""
+    import random
+
+    import flr_cpu
+    import hebatch_oracle as ho
+    rows, features = 48, 12
+    ids, X, y = flr.make_synthetic(rows, features, seed=11)
+    guest, host = flr.vertical_split(ids, X, y, 2)
+    keys = paillier.keygen(1024, paillier.default_rng(7), allow_insecure=True)
+    fed = flr.HeteroFederation(guest, host, [np.arange(rows)], np.arange(rows), keys, flr.FlrConfig(0.15, rows, seed=4))
+    okey = ho.Key(keys.public.n, keys.private.p, keys.private.q)
+    ref = flr_cpu.CpuHeteroFlr(okey, guest.X, guest.y, host.X, 0.15, 4)
+    for _ in range(3):
+        assert fed.run_epoch().loss == ref.run_iteration()
+    assert fed.decrypted == ref.decrypted
+    assert fed.combined_theta().tolist() == np.concatenate([ref.guest_theta, ref.host_theta]).tolist()

@@ -199,3 +199,17 @@ def test_hafb_roundtrips_and_reference_bytes():
         blob = bufferpool.serialize_to_bytes(batch)
         assert blob == ho.hafb_serialize(pk.key_bits, shape, exps, batch.payload, shared)
         assert bufferpool.deserialize(blob, pk) == batch
+
+
+def test_full_batch_row_selection_skips_the_copy():
+    """flr.HeteroFederation._take: X[idx] without the gather when idx is every row in order, a copy otherwise."""
+    import numpy as np
+    from paper_2107_13797_b200.flr import HeteroFederation
+    X = np.arange(12.0).reshape(6, 2)
+    assert HeteroFederation._take(X, np.arange(6)) is X
+    for idx in (np.array([0, 1, 2, 3, 5, 4]), np.arange(5), np.array([0, 2, 4]), np.array([5, 4, 3, 2, 1, 0]),
+                np.array([0, 1, 2, 2, 4, 5])):
+        got = HeteroFederation._take(X, idx)
+        assert got is not X and np.array_equal(got, X[idx])
+    y = np.arange(6.0)
+    assert HeteroFederation._take(y, np.arange(6)) is y
