@@ -68,8 +68,8 @@ int hb_ctx_set_private(hb_ctx* ctx, const uint32_t* p, const uint32_t* q, const 
 void hb_ctx_destroy(hb_ctx* ctx);
 /* Per-context tunables.  HB_OPT_MATVEC_WINDOW_BITS: bucket window of hb_matvec (2..13; 0 = by row count, the
  * default) -- lets tests exercise every width.  HB_OPT_POOL_KEEP_BYTES: how much freed scratch the library's pool on
- * the context's device keeps across synchronisations (default: 1 GiB or 1/16 of the device's memory, whichever is
- * larger -- 11 GiB on a 180 GB B200; shared by the contexts on that device).
+ * the context's device keeps across synchronisations (default: 1 GiB or 1/8 of the device's memory, whichever is
+ * larger -- 22 GiB on a 180 GB B200; shared by the contexts on that device).
  * HB_OPT_MATVEC_BLOCK_ROWS: rows of the inner dimension hb_matvec reduces per bucket pass (0 = 2^21, the default);
  * taller matrices are processed block by block and the blocks' partial products multiplied together. */
 enum hb_option { HB_OPT_MATVEC_WINDOW_BITS = 1, HB_OPT_POOL_KEEP_BYTES = 2, HB_OPT_MATVEC_BLOCK_ROWS = 3 };

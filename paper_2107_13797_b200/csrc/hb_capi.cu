@@ -31,15 +31,17 @@ cudaMemPool_t device_pool(int device) {
   props.location.id = device;
   cudaMemPool_t pool = nullptr;
   if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) { cudaGetLastError(); return nullptr; }
-  // Freed scratch kept across synchronisations: 1 GiB, or a sixteenth of the device's memory when that is more
-  // (11 GiB on a 180 GB B200).  A 1M-row encrypted matvec takes ~6 GB of bucket scratch per call; with less kept,
-  // every call pays the driver for fresh physical memory (measured: 2.2 s against 1.8 s per 1M x 100 matvec).
+  // Freed scratch kept across synchronisations: 1 GiB, or an eighth of the device's memory when that is more
+  // (22 GiB on a 180 GB B200).  A 1M-row encrypted matvec takes 9 GB of bucket scratch per call and the scalar
+  // powers of the same FLR iteration another 3 GB; with less kept, every call pays the driver for fresh physical
+  // memory (measured: 2.2 s against 1.8 s per 1M x 100 matvec with 1 GiB kept; inside a 1M-row FLR iteration
+  // 2.29 s per matvec with 11 GiB kept, 2.03 s with 40 GiB).
   unsigned long long keep = kPoolKeepDefault;
   size_t free_b = 0, total_b = 0;
   int cur = -1;
   cudaGetDevice(&cur);
   if (cudaSetDevice(device) == cudaSuccess && cudaMemGetInfo(&free_b, &total_b) == cudaSuccess)
-    keep = std::max<unsigned long long>(keep, (unsigned long long)total_b / 16);
+    keep = std::max<unsigned long long>(keep, (unsigned long long)total_b / 8);
   if (cur >= 0) cudaSetDevice(cur);
   cudaGetLastError();
   cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);

@@ -447,3 +447,23 @@ def test_multi_device_flr_epoch_equals_single_device(multi):
         out = fed.run(2)
         runs[label] = ([r.loss for r in out], fed.combined_theta().tolist(), fed.decrypted, out[-1].ledger)
     assert runs["one"] == runs["multi"]
+
+
+@pytest.mark.parametrize("name", ["k1024", "k2048", "k3072"])
+def test_codec_sector_paths_far_from_word_zero(okeys, name):
+    """The 32-byte-sector codec kernels with the magnitude words far above word 0: at exponents -70 ... -127 the
+    three words of uniform(-100, 100) values sit in sectors 1 to 2 -- warps whose 32 elements agree on the sector take
+    the write-once path with a shifted sector, the others the background-and-patch path; negative residues borrow
+    against words of n that are not the low ones.  Encode against the oracle, decode (generic kernel: magnitudes
+    beyond 2^96) back to the same doubles."""
+    ok = okeys(name)
+    pk, _sk = product_keys(ok)
+    rng = random.Random(5)
+    vals = [rng.uniform(-100.0, 100.0) for _ in range(150)] + [0.0, -0.0, 64.0, -64.0, 2.0 ** -20, -3.0 * 2.0 ** -18]
+    same_word = [float(rng.randrange(2 ** 20, 2 ** 21)) * (1 if i % 2 else -1) for i in range(96)]   # one ws for all
+    for exponent in (-70, -81, -100, -127):
+        for batch in (vals, same_word):
+            want = [ho.encode(ok, v, exponent)[0] for v in batch]
+            got = ops.batch_encode(pk, batch, exponent)
+            assert list(got.mantissas) == want, (name, exponent)
+            assert ops.batch_decode(pk, got) == [ho.decode(ok, m, exponent) for m in want]

@@ -60,6 +60,7 @@ def main():
     ap.add_argument("--features", type=int, default=200)
     ap.add_argument("--iters", type=int, default=2)
     ap.add_argument("--key-bits", type=int, default=2048)
+    ap.add_argument("--pool-keep-gib", type=float, default=0.0, help="HB_OPT_POOL_KEEP_BYTES for the key's context")
     ap.add_argument("--profile", action="store_true")
     ap.add_argument("--profile-first", action="store_true", help="cProfile the FIRST iteration instead of the last")
     args = ap.parse_args()
@@ -85,6 +86,9 @@ def main():
     ids, X, y = flr.make_synthetic(args.rows, args.features, seed=42)
     guest, host = flr.vertical_split(ids, X, y, 2)
     keys = paillier.keygen(args.key_bits, paillier.default_rng(7), allow_insecure=True)
+    if args.pool_keep_gib:
+        from paper_2107_13797_b200 import _native, device
+        device.context_for(keys.public.n).set_option(_native.HB_OPT_POOL_KEEP_BYTES, int(args.pool_keep_gib * 2 ** 30))
     full = [np.arange(args.rows)]
     fed = flr.HeteroFederation(guest, host, full, np.arange(args.rows), keys,
                                flr.FlrConfig(0.15, args.rows, seed=42))
