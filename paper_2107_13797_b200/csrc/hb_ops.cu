@@ -410,16 +410,25 @@ int matvec_finish(hb_ctx* ctx, const uint32_t* ab, bool invert, int d, uint32_t*
 
 // One encrypted row (digit-form bases) against a compact scalar matrix.  No host synchronisation except the
 // inversion flag at the very end, and that only when a scalar is negative.
-int matvec_row(hb_ctx* ctx, const uint32_t* cm, const PrepOut& pr, uint32_t* out, bool out_mont, long inner, int d,
-               cudaStream_t stream) {
+// One output row.  `status` (may be null when no scalar is negative) is the caller's inversion flag: it is set, never
+// cleared, so several rows share one flag and the caller looks at it once (check_status) after the last row.
+int matvec_row_async(hb_ctx* ctx, const uint32_t* cm, const PrepOut& pr, uint32_t* out, bool out_mont, long inner,
+                     int d, cudaStream_t stream, int* status) {
   Scratch sc(ctx, stream);
   uint32_t* ab = nullptr;
   int rc = matvec_ab_blocks(ctx, cm, pr, inner, d, sc, stream, &ab);
   if (rc) return rc;
+  return matvec_finish(ctx, ab, pr.nneg > 0, d, out, out_mont, sc, stream, status);
+}
+
+int matvec_row(hb_ctx* ctx, const uint32_t* cm, const PrepOut& pr, uint32_t* out, bool out_mont, long inner, int d,
+               cudaStream_t stream) {
+  Scratch sc(ctx, stream);
   int* status = nullptr;
   const bool invert = pr.nneg > 0;
+  int rc = HB_OK;
   if (invert) { rc = new_status(sc, stream, &status); if (rc) return rc; }
-  rc = matvec_finish(ctx, ab, invert, d, out, out_mont, sc, stream, status);
+  rc = matvec_row_async(ctx, cm, pr, out, out_mont, inner, d, stream, status);
   if (rc) return rc;
   return invert ? check_status(status, stream) : HB_OK;
 }
@@ -564,11 +573,15 @@ int hb_matvec_rep(hb_ctx* ctx, const uint32_t* c, const uint32_t* k, uint32_t* o
     const uint32_t* cm = nullptr;
     rc = as_mont(ctx, c, c_mont, rows * inner, sc, stream, &cm);
     if (rc) return rc;
+    // every output row is enqueued behind the previous one; the inversion flag is read once, after the last
+    int* status = nullptr;
+    if (pr.nneg > 0) { rc = new_status(sc, stream, &status); if (rc) return rc; }
     for (int64_t i = 0; i < rows; i++) {
-      rc = matvec_row(ctx, cm + (size_t)i * inner * L, pr, out + i * d * ow, out_mont, inner, (int)d, stream);
+      rc = matvec_row_async(ctx, cm + (size_t)i * inner * L, pr, out + i * d * ow, out_mont, inner, (int)d, stream,
+                            status);
       if (rc) return rc;
     }
-    return HB_OK;
+    return status ? check_status(status, stream) : HB_OK;
   }
   // General path (scalars wider than 64 bits, e.g. overflow-band residues): every term is an
   // independent power, then a strided product per output column.

@@ -467,3 +467,38 @@ def test_codec_sector_paths_far_from_word_zero(okeys, name):
             got = ops.batch_encode(pk, batch, exponent)
             assert list(got.mantissas) == want, (name, exponent)
             assert ops.batch_decode(pk, got) == [ho.decode(ok, m, exponent) for m in want]
+
+
+@pytest.mark.parametrize("name", ["k128", "k1024"])
+def test_matmul_2d_left_operand_bucket_path(okeys, name):
+    """A 2-D encrypted left operand (3 x inner) times signed 40-bit scalars: every output row goes through the bucket
+    kernels, enqueued one behind the other with ONE inversion flag read after the last row.  Against the oracle; a
+    non-unit ciphertext in the LAST row under a negative scalar still raises ZeroDivisionError, under a non-negative
+    one it is a value."""
+    ok = okeys(name)
+    pk, _sk = product_keys(ok)
+    rng = random.Random(21)
+    rows, inner, d = 3, 37, 4
+    ms = [rng.randrange(ok.n) for _ in range(rows * inner)]
+    cpay = enc_oracle(ok, ms, 8)
+    ks = signed_scalars(ok, inner * d, rng)
+    a = CiphertextBatch(pk, (rows, inner), (-3,), cpay, True)
+    x = PlaintextBatch(pk, (inner, d), (-2,), ks, True)
+    out = ops.batch_matmul(pk, a, x)
+    rws = tuple(tuple(cpay[i * inner + t] for t in range(inner)) for i in range(rows))
+    cols = tuple(tuple(ks[t * d + j] for t in range(inner)) for j in range(d))
+    assert list(out.payload) == ho.k_dot(ok, rws, cols, [(i, j) for i in range(rows) for j in range(d)])
+    assert out.shape == (rows, d) and out.exponents == (-5,)
+    bad = list(cpay)
+    bad[-1] = ok.p                                              # not a unit mod n^2, last row, last term
+    neg_last = list(ks)
+    neg_last[(inner - 1) * d] = ok.n - 5                        # its scalar in column 0 is negative
+    with pytest.raises(ZeroDivisionError):
+        ops.batch_matmul(pk, CiphertextBatch(pk, (rows, inner), (-3,), bad, True),
+                         PlaintextBatch(pk, (inner, d), (-2,), neg_last, True))
+    pos = [k if k < ok.max_int else ok.n - k for k in ks]       # magnitudes only: nothing is inverted
+    got = ops.batch_matmul(pk, CiphertextBatch(pk, (rows, inner), (-3,), bad, True),
+                           PlaintextBatch(pk, (inner, d), (-2,), pos, True))
+    rws_bad = tuple(tuple(bad[i * inner + t] for t in range(inner)) for i in range(rows))
+    cols_pos = tuple(tuple(pos[t * d + j] for t in range(inner)) for j in range(d))
+    assert list(got.payload) == ho.k_dot(ok, rws_bad, cols_pos, [(i, j) for i in range(rows) for j in range(d)])
