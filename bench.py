@@ -657,12 +657,12 @@ def flr_cpu_extra(cpu_rows: int, gpu_iter_s: float, gpu_rows: int, features: int
 
 def _ncu_traffic_per_element():
     """dram bytes read + written per encrypted element, from the committed ncu --set full capture of k_encrypt
-    (profiles/r01e_ncu_summary.json; the capture ran 37888 elements).  Almost all of it is the per-warp window
+    (profiles/r02_ncu_summary.json; the capture ran 37888 elements).  Almost all of it is the per-warp window
     tables (33 slots x 4 KiB per warp, 160 MB for the grid: more than the L2 holds), not operand traffic -- about
     8 GB/s, a thousandth of the HBM bandwidth, under a multiplier-bound kernel."""
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
     try:
-        with open(os.path.join(ROOT, "profiles", "r01e_ncu_summary.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", "r02_ncu_summary.json")) as fh:
             enc = json.load(fh)["encrypt"]
         total = sum(float(enc[k]["value"]) * scale[enc[k]["unit"]] for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
         return total / 37888
