@@ -15,23 +15,36 @@ namespace {
 struct MT {
   uint32_t* s;
   int idx;
-  void refill() {
+  static inline uint32_t twist(uint32_t hi, uint32_t lo, uint32_t far) {
+    const uint32_t y = (hi & 0x80000000u) | (lo & 0x7fffffffu);
+    return far ^ (y >> 1) ^ ((0u - (y & 1u)) & 0x9908b0dfu);
+  }
+  void refill() {                        // three modulo-free stretches (the compiler vectorises the first two)
     constexpr int N = 624, M = 397;
-    constexpr uint32_t UP = 0x80000000u, LO = 0x7fffffffu, A = 0x9908b0dfu;
-    for (int k = 0; k < N; k++) {
-      uint32_t y = (s[k] & UP) | (s[(k + 1) % N] & LO);
-      s[k] = s[(k + M) % N] ^ (y >> 1) ^ ((y & 1u) ? A : 0u);
-    }
+    int k = 0;
+    for (; k < N - M; k++) s[k] = twist(s[k], s[k + 1], s[k + M]);
+    for (; k < N - 1; k++) s[k] = twist(s[k], s[k + 1], s[k + M - N]);
+    s[N - 1] = twist(s[N - 1], s[0], s[M - 1]);
     idx = 0;
   }
-  uint32_t next() {
-    if (idx >= 624) refill();
-    uint32_t y = s[idx++];
+  static inline uint32_t temper(uint32_t y) {
     y ^= y >> 11;
     y ^= (y << 7) & 0x9d2c5680u;
     y ^= (y << 15) & 0xefc60000u;
     y ^= y >> 18;
     return y;
+  }
+  // the next `count` outputs, in order, into dst (refilling as the state runs out)
+  void fill(uint32_t* dst, int count) {
+    int done = 0;
+    while (done < count) {
+      if (idx >= 624) refill();
+      const int take = std::min(count - done, 624 - idx);
+      const uint32_t* src = s + idx;
+      for (int j = 0; j < take; j++) dst[done + j] = temper(src[j]);
+      idx += take;
+      done += take;
+    }
   }
 };
 
@@ -54,29 +67,21 @@ extern "C" int hb_mt19937_randrange1(uint32_t* state, int* index, const uint32_t
   const int k = top * 32 + (32 - __builtin_clz(bound[top]));     // (n - 1).bit_length()
   const int words = (k + 31) / 32;
   MT mt{state, *index};
-  std::vector<uint32_t> cand(wn, 0);
+  const int topshift = (k % 32) ? 32 - (k % 32) : 0;
   for (int64_t e = 0; e < count; e++) {
-    while (true) {
-      int left = k;
-      for (int i = 0; i < words; i++, left -= 32) {
-        uint32_t r = mt.next();
-        if (left < 32) r >>= (32 - left);
-        cand[i] = r;
-      }
-      // accept when cand < bound
-      bool below = false;
+    uint32_t* o = out + e * wn;
+    while (true) {                       // candidates are drawn straight into the output row
+      mt.fill(o, words);
+      o[words - 1] >>= topshift;
+      bool below = false;                // accept when candidate < bound
       for (int i = words - 1; i >= 0; i--) {
-        if (cand[i] != bound[i]) { below = cand[i] < bound[i]; break; }
+        if (o[i] != bound[i]) { below = o[i] < bound[i]; break; }
       }
       if (below) break;
     }
-    uint32_t* o = out + e * wn;
-    uint32_t carry = 1;
-    for (int i = 0; i < wn; i++) {
-      uint32_t v = (i < words ? cand[i] : 0u);
-      uint32_t s = v + carry;
-      carry = (s < v) ? 1u : 0u;
-      o[i] = s;
+    for (int i = words; i < wn; i++) o[i] = 0u;
+    for (int i = 0; i < wn; i++) {       // + 1
+      if (++o[i] != 0u) break;
     }
   }
   *index = mt.idx;

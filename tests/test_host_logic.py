@@ -213,3 +213,35 @@ def test_full_batch_row_selection_skips_the_copy():
         assert got is not X and np.array_equal(got, X[idx])
     y = np.arange(6.0)
     assert HeteroFederation._take(y, np.arange(6)) is y
+
+
+def test_native_draw_stream_equals_cpython_without_a_gpu():
+    """hb_mt19937_randrange1 is host code: CPython's randrange(1, n) stream reproduced word for word from getstate(),
+    across state refills, for moduli whose bit length is and is not a multiple of 32, and the generator state handed
+    back equals CPython's own after the same draws.  hb_secure_randrange1 (OS entropy): values in [1, n)."""
+    import ctypes
+    import random
+
+    import numpy as np
+    from paper_2107_13797_b200 import _native
+    lib = _native.lib()
+    for n in (35, 3, 2 ** 61 - 1, (1 << 100) + 7, (1 << 255) + 95, (1 << 2047) + 12345, (1 << 2048) - 159):
+        wn = (n.bit_length() + 31) // 32
+        n_words = np.frombuffer(n.to_bytes(4 * wn, "little"), dtype=np.uint32).copy()
+        rng = random.Random(n % 1000)
+        rng.random()                                              # start somewhere inside the state
+        saved = rng.getstate()
+        state = np.array(saved[1][:624], dtype=np.uint32)
+        index = ctypes.c_int(saved[1][624])
+        count = 700                                               # 700 x 64 words: dozens of refills
+        out = np.empty((count, wn), np.uint32)
+        _native.check(lib.hb_mt19937_randrange1(state.ctypes.data, ctypes.byref(index), n_words.ctypes.data, wn,
+                                                count, out.ctypes.data))
+        want = [rng.randrange(1, n) for _ in range(count)]
+        assert [int.from_bytes(r.tobytes(), "little") for r in out] == want
+        after = rng.getstate()[1]
+        assert tuple(int(v) for v in state) == after[:624] and index.value == after[624]
+        _native.check(lib.hb_secure_randrange1(n_words.ctypes.data, wn, count, out.ctypes.data))
+        got = [int.from_bytes(r.tobytes(), "little") for r in out]
+        assert all(1 <= v < n for v in got)
+        assert n < 100 or len(set(got)) > count // 2
