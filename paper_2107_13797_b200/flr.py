@@ -288,7 +288,7 @@ class HomoFederation:
 
     def _send(self, party, values) -> tuple:
         """Encode at the protocol exponent, encrypt with the party's stream, ship as HAFB bytes."""
-        plain = _encode(self.pk, [float(v) for v in values], HOMO_GRADIENT_EXPONENT)
+        plain = _encode(self.pk, [float(v) for v in values], HOMO_GRADIENT_EXPONENT, self.backend)
         cipher = operators.batch_encrypt(self.pk, plain, party["rng"], self.backend)
         return serialize_to_bytes(cipher), len(party["X"])
 
@@ -303,10 +303,10 @@ class HomoFederation:
         acc = None
         for wire, rows in wires:                                          # parties.py:422-428
             cipher = deserialize(wire, pk)
-            weight = encode_batch(pk, [float(rows)], target_exponent=0)
+            weight = encode_batch(pk, [float(rows)], target_exponent=0, backend=be)
             weighted = operators.batch_mul_plain(pk, cipher, weight, be)
             acc = weighted if acc is None else operators.batch_add(pk, acc, weighted, be)
-        aggregated = np.asarray(decode_batch(pk, operators.batch_decrypt(self.keys.private, acc, be))) / total_rows
+        aggregated = np.asarray(decode_batch(pk, operators.batch_decrypt(self.keys.private, acc, be), be)) / total_rows
         self.aggregated_gradients.append(aggregated)
         self.theta = self.theta - self.config.learning_rate * aggregated
         loss_acc = None
@@ -315,7 +315,7 @@ class HomoFederation:
             total = float(np.sum(LOG2 - 0.5 * party["y"] * z + 0.125 * z * z))
             cipher = deserialize(self._send(party, [total])[0], pk)
             loss_acc = cipher if loss_acc is None else operators.batch_add(pk, loss_acc, cipher, be)
-        loss = decode_batch(pk, operators.batch_decrypt(self.keys.private, loss_acc, be))[0] / total_rows
+        loss = decode_batch(pk, operators.batch_decrypt(self.keys.private, loss_acc, be), be)[0] / total_rows
         self.epoch += 1
         return EpochResult(self.epoch, loss, float(np.linalg.norm(aggregated)), TransferLedger().to_json())
 

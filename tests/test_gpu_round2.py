@@ -502,3 +502,18 @@ def test_matmul_2d_left_operand_bucket_path(okeys, name):
     rws_bad = tuple(tuple(bad[i * inner + t] for t in range(inner)) for i in range(rows))
     cols_pos = tuple(tuple(pos[t * d + j] for t in range(inner)) for j in range(d))
     assert list(got.payload) == ho.k_dot(ok, rws_bad, cols_pos, [(i, j) for i in range(rows) for j in range(d)])
+
+
+def test_multi_device_homo_aggregation_equals_single_device(multi):
+    """The horizontal protocol (BASELINE configs[4] shape, reduced) with the multi-device backend passed in: same
+    aggregated gradients, model and loss as the single-device run."""
+    from paper_2107_13797_b200 import flr
+    keys = paillier.keygen(512, paillier.default_rng(5), allow_insecure=True)
+    ids, X, y = flr.make_synthetic(90, 40, seed=2)
+    runs = {}
+    for label, be in (("one", CudaBackend()), ("multi", multi)):
+        parts = flr.horizontal_split(ids, X, y, 3)
+        fed = flr.HomoFederation(parts, keys, flr.FlrConfig(learning_rate=0.15, seed=6), backend=be)
+        out = fed.run(2)
+        runs[label] = ([r.loss for r in out], fed.theta.tolist(), [g.tolist() for g in fed.aggregated_gradients])
+    assert runs["one"] == runs["multi"]
