@@ -275,20 +275,33 @@ def run_b200(args):
         raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # Rehearsal of the multi-rank code path on a box with fewer GPUs than ranks (development only; the numbers mean
+    # nothing): HB_BENCH_SHARE_DEVICES=1 maps rank r to device r mod device_count and the collectives go over gloo
+    # on host tensors, because NCCL refuses two ranks on one device.
+    rehearsal = os.environ.get("HB_BENCH_SHARE_DEVICES", "") not in ("", "0")
+    ndev = torch.cuda.device_count()
+    if local >= ndev and not rehearsal:
+        raise SystemExit(f"rank {rank} needs CUDA device {local}, the box has {ndev}")
+    local = local % ndev
     torch.cuda.set_device(local)
     dist = None
+    comm_dev = "cpu" if rehearsal else "cuda"
     if world > 1:
         import torch.distributed as dist_mod
         dist = dist_mod
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if rehearsal:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     def barrier():
+        torch.cuda.synchronize()
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
 
     def max_over_ranks(x: float) -> float:
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device=comm_dev)
         if dist is not None:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
@@ -411,9 +424,10 @@ def run_b200(args):
                 return
             # rows are sharded: per-rank partial pairs, NCCL all-gather (d x 2 ciphertexts per rank), combine
             _native.check(lib.hb_matvec_partial(ctx.handle, c.data_ptr(), xk.data_ptr(), ab.data_ptr(), inner, d, stream))
-            parts = [torch.empty_like(ab) for _ in range(world)]
-            dist.all_gather(parts, ab)
-            allab = torch.cat(parts, dim=0).contiguous()
+            mine = ab.to(comm_dev)
+            parts = [torch.empty_like(mine) for _ in range(world)]
+            dist.all_gather(parts, mine)
+            allab = torch.cat(parts, dim=0).to("cuda").contiguous()
             _native.check(lib.hb_matvec_combine(ctx.handle, allab.data_ptr(), world, mv.data_ptr(), d, stream))
 
         matvec_once()
@@ -537,7 +551,8 @@ def run_b200(args):
     if not args.no_flr and count >= 100_000:
         if world > 1:
             time.sleep(2.0)                      # the other ranks are leaving their GPUs
-        devices = [int(v) for v in args.flr_devices.split(",")] if args.flr_devices else list(range(world))
+        devices = ([int(v) for v in args.flr_devices.split(",")] if args.flr_devices
+                   else [d % ndev for d in range(world)])
         extras.update(flr_extra(args.flr_rows, devices, args.flr_iters))
         if args.flr_cpu_rows > 0:
             extras.update(flr_cpu_extra(args.flr_cpu_rows, extras["flr_hetero_iter_s"], args.flr_rows))
@@ -575,6 +590,8 @@ def run_b200(args):
                    "l2": "inputs per step (1 GiB) exceed the 126 MB L2; no explicit flush",
                    "oracle_check": f"{cpu['sample']} strided elements: ciphertexts and decryptions bit-identical "
                                    "to the CPU oracle"},
+        **({"rehearsal": "ranks share devices, gloo collectives: code-path check only, not a measurement"}
+           if rehearsal else {}),
         "clocks": clocks, "e2e": e2e, "e2e_operator_api": api, "gpu_launches": launches, "roofline": roofline,
         "cpu_baseline": {"value": cpu["ops_per_s"], "unit": "ops/s", "cores": cpu["threads"], "kind": "port",
                          "sample": f"{cpu['sample']} encrypt + {cpu['sample']} decrypt of the benchmarked batch, GMP "

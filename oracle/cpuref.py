@@ -29,7 +29,13 @@ def lib():
 
 
 def threads() -> int:
-    return int(lib().cpuref_threads())
+    """Host threads the CPU baseline uses: every core this process may run on.  Deliberately NOT OpenMP's default:
+    torchrun exports OMP_NUM_THREADS=1 to its ranks, which would silently turn the "all host cores" baseline into a
+    one-core one; the num_threads clause of cpu_ref.c's parallel regions overrides that variable."""
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except AttributeError:
+        return max(1, os.cpu_count() or 1)
 
 
 def _w(vals, width):
