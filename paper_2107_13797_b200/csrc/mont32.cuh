@@ -635,8 +635,25 @@ struct Mont {
     finish(r, E, O, pend_lo, pend_hi);
   }
 
-  // limbs [t*LPT, (t+1)*LPT) of the little-endian word array w[0..nwords) (zero beyond it)
+  // limbs [t*LPT, (t+1)*LPT) of the little-endian word array w[0..nwords) (zero beyond it).
+  // Element arrays are read and written 16 bytes at a time whenever the word count allows it (every key size that is
+  // a multiple of 64 bits): a lane's limbs are contiguous, so one LDG.128 replaces four LDG.32 that would each touch
+  // a different sector per lane -- k_mulmod was bound by those L1 wavefronts, not by the multiplier.  Taken when the
+  // element base is 16-byte aligned (device allocations are; word counts that are multiples of 4 keep
+  // every element aligned; anything else takes the word-by-word path).
   __device__ __forceinline__ void load_words(uint32_t (&r)[LPT], const uint32_t* __restrict__ w, int nwords) const {
+    if constexpr (LPT % 4 == 0) {
+      if ((nwords & 3) == 0 && (reinterpret_cast<uintptr_t>(w) & 15) == 0) {
+#pragma unroll
+        for (int j = 0; j < LPT / 4; j++) {
+          const int k = t * LPT + 4 * j;
+          uint4 v = make_uint4(0u, 0u, 0u, 0u);
+          if (k < nwords) v = *reinterpret_cast<const uint4*>(w + k);
+          r[4 * j] = v.x; r[4 * j + 1] = v.y; r[4 * j + 2] = v.z; r[4 * j + 3] = v.w;
+        }
+        return;
+      }
+    }
 #pragma unroll
     for (int i = 0; i < LPT; i++) {
       const int k = t * LPT + i;
@@ -645,20 +662,46 @@ struct Mont {
   }
   __device__ __forceinline__ void store_words(uint32_t* __restrict__ w, int nwords, const uint32_t (&r)[LPT],
                                               bool valid = true) const {
+    if constexpr (LPT % 4 == 0) {
+      if ((nwords & 3) == 0 && (reinterpret_cast<uintptr_t>(w) & 15) == 0) {
+#pragma unroll
+        for (int j = 0; j < LPT / 4; j++) {
+          const int k = t * LPT + 4 * j;
+          if (valid && k < nwords)
+            *reinterpret_cast<uint4*>(w + k) = make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
+        }
+        return;
+      }
+    }
 #pragma unroll
     for (int i = 0; i < LPT; i++) {
       const int k = t * LPT + i;
       if (valid && k < nwords) w[k] = r[i];
     }
   }
-  // full L-limb arrays (constants, scratch)
+  // full L-limb arrays (constants, scratch, Montgomery digit form): always 16-byte accesses
   __device__ __forceinline__ void load_limbs(uint32_t (&r)[LPT], const uint32_t* __restrict__ d) const {
+    if constexpr (LPT % 4 == 0) {
+      const uint4* p = reinterpret_cast<const uint4*>(d + t * LPT);
 #pragma unroll
-    for (int i = 0; i < LPT; i++) r[i] = d[t * LPT + i];
+      for (int j = 0; j < LPT / 4; j++) {
+        const uint4 v = p[j];
+        r[4 * j] = v.x; r[4 * j + 1] = v.y; r[4 * j + 2] = v.z; r[4 * j + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < LPT; i++) r[i] = d[t * LPT + i];
+    }
   }
   __device__ __forceinline__ void store_limbs(uint32_t* __restrict__ d, const uint32_t (&r)[LPT]) const {
+    if constexpr (LPT % 4 == 0) {
+      uint4* p = reinterpret_cast<uint4*>(d + t * LPT);
 #pragma unroll
-    for (int i = 0; i < LPT; i++) d[t * LPT + i] = r[i];
+      for (int j = 0; j < LPT / 4; j++) p[j] = make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < LPT; i++) d[t * LPT + i] = r[i];
+    }
   }
 };
 
