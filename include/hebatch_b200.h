@@ -27,6 +27,8 @@
  *     digit form x * R mod n^2 (hb_ct_limbs per element), the form chained operators keep in HBM so that an
  *     addition is one modular multiplication and no operator converts in and out.  The *_rep entry points take
  *     `flags` built from HB_A_MONT / HB_B_MONT / HB_OUT_MONT; the classic names are the all-plain case.
+ *     Digit-form arrays must be 16-byte aligned (HB_ERR_ARG otherwise); plain-word arrays may have any alignment
+ *     (16-byte aligned ones are moved 16 bytes at a time).
  *   - *_host functions take HOST pointers, stage through pinned buffers on side streams (chunked,
  *     copy/compute overlapped) and return when the result is in the caller's buffer.
  *   - Return value: 0 on success, negative hb_status on failure; hb_last_error() gives the text

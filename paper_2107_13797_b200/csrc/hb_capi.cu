@@ -66,6 +66,8 @@ int encrypt_common(hb_ctx* ctx, const uint32_t* m, const uint32_t* c, const uint
   if (!ctx || !r || !out || (mode == 0 ? !m : !c)) return fail(HB_ERR_ARG, "null pointer");
   if (count < 0) return fail(HB_ERR_ARG, "negative count");
   if (count == 0) return HB_OK;
+  HB_REQUIRE_ALIGNED16(c, mode == 1 && (flags & HB_A_MONT));
+  HB_REQUIRE_ALIGNED16(out, flags & HB_OUT_MONT);
   cudaStream_t stream = (cudaStream_t)stream_;
   CU(cudaSetDevice(ctx->device));
   const int cfg = ctx->cfg_pub;
@@ -109,6 +111,9 @@ int mulmod_common(hb_ctx* ctx, const uint32_t* a, const uint32_t* b, uint32_t* o
   A.a_mont = (flags & HB_A_MONT) ? 1 : 0;
   A.b_mont = (!lift && (flags & HB_B_MONT)) ? 1 : 0;
   A.out_mont = (flags & HB_OUT_MONT) ? 1 : 0;
+  HB_REQUIRE_ALIGNED16(a, A.a_mont);
+  HB_REQUIRE_ALIGNED16(b, A.b_mont);
+  HB_REQUIRE_ALIGNED16(out, A.out_mont);
   HB_DISPATCH(cfg, k_mulmod, l, stream, A)
   CU(cudaGetLastError());
   return HB_OK;
@@ -338,6 +343,8 @@ int hb_fore_gradient(hb_ctx* ctx, const uint32_t* c, const uint32_t* lg, const u
   A.count = count; A.wn = ctx->wn; A.wc = ctx->wc;
   A.c_mont = (flags & HB_A_MONT) ? 1 : 0;
   A.out_mont = (flags & HB_OUT_MONT) ? 1 : 0;
+  HB_REQUIRE_ALIGNED16(c, A.c_mont);
+  HB_REQUIRE_ALIGNED16(out, A.out_mont);
   HB_DISPATCH_ENC(cfg, k_fore_gradient, l, stream, A)
   CU(cudaGetLastError());
   CU(cudaFreeAsync(tbl, stream));
@@ -439,6 +446,7 @@ int hb_decrypt_rep(hb_ctx* ctx, const uint32_t* c, uint32_t* m_out, int64_t coun
   if (!ctx || !c || !m_out) return fail(HB_ERR_ARG, "null pointer");
   if (!ctx->has_private) return fail(HB_ERR_NOPRIVATE, "context has no private key");
   if (count <= 0) return count == 0 ? HB_OK : fail(HB_ERR_ARG, "negative count");
+  HB_REQUIRE_ALIGNED16(c, true);
   const int Lpub = kCfgs[ctx->cfg_pub].lpt * kCfgs[ctx->cfg_pub].tpi;
   const int Lpriv = kCfgs[ctx->cfg_priv].lpt * kCfgs[ctx->cfg_priv].tpi;
   // the kernel reads the digit form directly when the n^2 context's R is the square of the p^2 / q^2 context's

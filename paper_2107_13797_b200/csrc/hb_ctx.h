@@ -50,6 +50,11 @@ extern thread_local std::string g_err;
 extern std::atomic<long long> g_launches;
 
 inline int fail(int code, const std::string& msg) { g_err = msg; return code; }
+// Montgomery digit-form arrays are moved 16 bytes at a time (Mont::load_limbs / store_limbs): every element is a
+// multiple of 128 bytes, so only the base pointer can be off.
+#define HB_REQUIRE_ALIGNED16(ptr, is_digit_form)                                                        \
+  do { if ((is_digit_form) && (reinterpret_cast<uintptr_t>(ptr) & 15) != 0)                             \
+    return hbi::fail(HB_ERR_ARG, "Montgomery digit-form arrays must be 16-byte aligned"); } while (0)
 
 // The library's own stream-ordered memory pool on `device` (one per device and process, shared by the contexts on
 // it).  Scratch never comes from the device's default pool, whose attributes belong to the application.

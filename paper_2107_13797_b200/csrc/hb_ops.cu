@@ -61,6 +61,7 @@ int from_mont(hb_ctx* ctx, const uint32_t* dig, uint32_t* words, long count, cud
 // Digit form of a ciphertext operand: the caller's array when it already is (HB_*_MONT), a converted copy otherwise.
 int as_mont(hb_ctx* ctx, const uint32_t* c, bool is_mont, long count, Scratch& sc, cudaStream_t stream,
             const uint32_t** out) {
+  HB_REQUIRE_ALIGNED16(c, is_mont);
   if (is_mont) { *out = c; return HB_OK; }
   uint32_t* cm = nullptr;
   CU(sc.get(&cm, (size_t)count * Ldig(ctx->cfg_pub)));
@@ -170,6 +171,8 @@ int pow_window(int bits) { return bits <= 6 ? 1 : bits <= 24 ? 2 : bits <= 96 ? 
 // out[e] = pow_scalar(c[e / c_div], k[e % k_period]) for e < count
 int powscalar_impl(hb_ctx* ctx, const uint32_t* c, bool c_mont, long ncipher, long c_div, const uint32_t* k,
                    long k_period, int raw, uint32_t* out, bool out_mont, long count, cudaStream_t stream) {
+  HB_REQUIRE_ALIGNED16(c, c_mont);
+  HB_REQUIRE_ALIGNED16(out, out_mont);
   const int cfg = ctx->cfg_pub;
   const int L = Ldig(cfg);
   Scratch sc(ctx, stream);
@@ -219,6 +222,8 @@ int powscalar_impl(hb_ctx* ctx, const uint32_t* c, bool c_mont, long ncipher, lo
 // win: words per plain input element (wc, or wn for plaintext-width values); ignored for digit-form input.
 int product_impl(hb_ctx* ctx, const uint32_t* c, int win, bool in_mont, uint32_t* out, bool out_mont, long ngroups,
                  long glen, long gstride, long estride, cudaStream_t stream) {
+  HB_REQUIRE_ALIGNED16(c, in_mont);
+  HB_REQUIRE_ALIGNED16(out, out_mont);
   const int cfg = ctx->cfg_pub;
   const int L = Ldig(cfg);
   Scratch sc(ctx, stream);
@@ -463,6 +468,8 @@ int hb_ct_convert(hb_ctx* ctx, const uint32_t* in, uint32_t* out, int64_t count,
   if (count < 0) return fail(HB_ERR_ARG, "negative count");
   if (count == 0) return HB_OK;
   CU(cudaSetDevice(ctx->device));
+  HB_REQUIRE_ALIGNED16(out, to_montgomery != 0);
+  HB_REQUIRE_ALIGNED16(in, to_montgomery == 0);
   return to_montgomery ? to_mont(ctx, in, ctx->wc, out, count, (cudaStream_t)stream_)
                        : from_mont(ctx, in, out, count, (cudaStream_t)stream_);
 }

@@ -517,3 +517,34 @@ def test_multi_device_homo_aggregation_equals_single_device(multi):
         out = fed.run(2)
         runs[label] = ([r.loss for r in out], fed.theta.tolist(), [g.tolist() for g in fed.aggregated_gradients])
     assert runs["one"] == runs["multi"]
+
+
+def test_misaligned_digit_form_pointer_is_rejected(okeys):
+    """Montgomery digit-form arrays are moved 16 bytes at a time: a base pointer that is not 16-byte aligned is an
+    argument error, not a fault; plain-word arrays of any alignment still work (word path)."""
+    t = device.torch()
+    ok = okeys("k512")
+    pk, sk = product_keys(ok)
+    ctx = device.context_for(ok.n)
+    lib = _native.lib()
+    count = 5
+    c = ops.batch_encrypt(pk, encode_batch(pk, [1.0, -2.0, 3.5, 0.25, -7.0], target_exponent=-4), random.Random(4),
+                          CudaBackend(resident_montgomery=False))
+    plain = c.words.device()
+    buf = t.zeros((count * ctx.limbs + 4,), dtype=t.int32, device="cuda")
+    stream = device.current_stream_ptr()
+    with pytest.raises(ValueError):
+        _native.check(lib.hb_ct_convert(ctx.handle, plain.data_ptr(), buf.data_ptr() + 4, count, 1, stream))
+    _native.check(lib.hb_ct_convert(ctx.handle, plain.data_ptr(), buf.data_ptr(), count, 1, stream))
+    with pytest.raises(ValueError):
+        _native.check(lib.hb_mulmod_rep(ctx.handle, buf.data_ptr() + 4, buf.data_ptr(), buf.data_ptr(), count, 0,
+                                        _native.HB_A_MONT | _native.HB_B_MONT | _native.HB_OUT_MONT, stream))
+    # plain words at a 4-byte offset: accepted, same bits as the aligned call
+    shifted = t.zeros((count * ctx.wc + 1,), dtype=t.int32, device="cuda")
+    shifted[1:] = plain.reshape(-1)
+    out_a = t.empty((count, ctx.wc), dtype=t.int32, device="cuda")
+    out_b = t.empty((count, ctx.wc), dtype=t.int32, device="cuda")
+    _native.check(lib.hb_mulmod(ctx.handle, plain.data_ptr(), plain.data_ptr(), out_a.data_ptr(), count, 0, stream))
+    _native.check(lib.hb_mulmod(ctx.handle, shifted.data_ptr() + 4, shifted.data_ptr() + 4, out_b.data_ptr(), count, 0,
+                                stream))
+    assert t.equal(out_a, out_b)
