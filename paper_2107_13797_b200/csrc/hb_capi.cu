@@ -393,7 +393,7 @@ int hb_sqrmod(hb_ctx* ctx, const uint32_t* a, uint32_t* out, int64_t count, int 
   hb::SqrArgs A;
   A.mod = dev_mod(ctx->d_pub, ctx->mod_n2);
   A.a = a; A.out = out; A.count = count; A.wc = ctx->wc; A.reps = reps;
-#ifdef HB_DEV_ONLY_3072
+#if defined(HB_DEV_ONLY_3072) || defined(HB_DEV_ONLY_2048)
   return fail(HB_ERR_UNSUPPORTED, "development build");
 #else
   HB_DISPATCH_SQR(cfg, k_sqrmod, l, stream, A)

@@ -27,6 +27,16 @@ struct ModDev {
 __host__ __device__ constexpr int blocks_per_sm(int lpt) {
   return lpt > 32 ? HB_NS_BLOCKS : lpt > 24 ? 2 : lpt > 20 ? 3 : lpt <= 8 ? 6 : 4;
 }
+// Resident blocks per scheduler-quad for the encrypt / obfuscate kernel alone.  -DHB_SF32 (experiment): the (32,4)
+// shape takes its multiplier operand from shared memory like (48,4) does, which frees 32 registers per thread and
+// lets a third warp per scheduler fit (168 registers).
+#ifdef HB_SF32
+__host__ __device__ constexpr int enc_blocks_per_sm(int lpt) { return lpt == 32 ? 3 : blocks_per_sm(lpt); }
+__host__ __device__ constexpr bool enc_stages_operand(int lpt) { return lpt == 48 || lpt == 32; }
+#else
+__host__ __device__ constexpr int enc_blocks_per_sm(int lpt) { return blocks_per_sm(lpt); }
+__host__ __device__ constexpr bool enc_stages_operand(int lpt) { return lpt == 48; }
+#endif
 template <int LPT>
 __device__ __forceinline__ void tile_store(uint32_t* tw, int e, const uint32_t (&x)[LPT]) {
   int lane = threadIdx.x & 31;
@@ -172,7 +182,7 @@ inline Launch plan(const hb_ctx* ctx, int base, long count, bool encrypt_kernel 
   const int ipw = 32 / tpi;
   long ntiles = (count + ipw - 1) / ipw;
   long nwarps = ntiles;
-  const long maxw = (long)ctx->sms * hb::blocks_per_sm(lpt) * 4;
+  const long maxw = (long)ctx->sms * (encrypt_kernel ? hb::enc_blocks_per_sm(lpt) : hb::blocks_per_sm(lpt)) * 4;
   if (nwarps > maxw) nwarps = maxw;
   if (nwarps < 1) nwarps = 1;
   // One warp per block (4 * blocks_per_sm of them resident per SM): the grid-stride tile loop of every kernel then
@@ -225,7 +235,18 @@ constexpr size_t sqr_smem_bytes() { return (size_t)hb::Mont<LPT, TPI>::SQ_WORDS 
 #endif
 
 // k_encrypt: the nine shapes; (48, 4) takes its operand staging area and the modulus copy as dynamic shared memory.
+#ifdef HB_SF32
+#define HB_ENC_SF32_CASE(KERNEL, launch, stream, args)                                                  \
+  if (launch.cfg == 3) {                                                                                \
+    hb::KERNEL<32, 4><<<launch.blocks, launch.threads,                                                  \
+                        hb::Mont<32, 4>::NS_SMEM_WORDS * sizeof(uint32_t), stream>>>(args);               \
+    hbi::g_launches++;                                                                                  \
+  } else
+#else
+#define HB_ENC_SF32_CASE(KERNEL, launch, stream, args)
+#endif
 #define HB_DISPATCH_ENC(cfg, KERNEL, launch, stream, args)                                              \
+  HB_ENC_SF32_CASE(KERNEL, launch, stream, args)                                                        \
   if (launch.cfg == 8) {                                                                                \
     hb::KERNEL<48, 4><<<launch.blocks, launch.threads,                                                  \
                         hb::Mont<48, 4>::NS_SMEM_WORDS * sizeof(uint32_t), stream>>>(args);               \
@@ -234,7 +255,15 @@ constexpr size_t sqr_smem_bytes() { return (size_t)hb::Mont<LPT, TPI>::SQ_WORDS 
     HB_DISPATCH_POW(cfg, KERNEL, launch, stream, args)                                                  \
   }
 
-#ifdef HB_DEV_ONLY_3072   /* development builds: only the shapes a 3072-bit key uses, for quick A/B experiments */
+#if defined(HB_DEV_ONLY_2048)   /* development builds: only the shapes a 2048-bit key uses at throughput counts */
+#define HB_DISPATCH(cfg, KERNEL, launch, stream, args)                                           \
+  switch (launch.cfg) {                                                                                 \
+    case 1: hb::KERNEL<16, 4><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break; \
+    case 3: hb::KERNEL<32, 4><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break; \
+    default: return hbi::fail(HB_ERR_UNSUPPORTED, "no limb configuration");                            \
+  }                                                                                              \
+  hbi::g_launches++;
+#elif defined(HB_DEV_ONLY_3072)   /* development builds: only the shapes a 3072-bit key uses, for quick A/B experiments */
 #define HB_DISPATCH(cfg, KERNEL, launch, stream, args)                                           \
   switch (launch.cfg) {                                                                                 \
     case 2: hb::KERNEL<24, 4><<<launch.blocks, launch.threads, launch.smem, stream>>>(args); break; \

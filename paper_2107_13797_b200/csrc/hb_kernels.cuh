@@ -35,7 +35,7 @@ __device__ __forceinline__ void run_prog(const Mont<LPT, TPI>& mt, uint32_t (&x)
     if (kind == OP_LOAD) {
       tile_load<LPT>(tw, src, x);
     } else if (kind != OP_KEEP) {
-      if constexpr (LPT == 48) {              // wide-lane shape: b comes from shared memory (Mont::mul_sf)
+      if constexpr (enc_stages_operand(LPT)) {  // wide-lane shape: b comes from shared memory (Mont::mul_sf)
         uint32_t y[LPT];
         if (kind == OP_MUL) {
           tile_load<LPT>(tw, src, y);
@@ -76,7 +76,7 @@ extern __shared__ __align__(16) uint32_t hb_dyn_smem[];
 template <int LPT, int TPI>
 __device__ __forceinline__ uint32_t* sqr_scratch() {
   using M = Mont<LPT, TPI>;
-  if constexpr (LPT == 48) {
+  if constexpr (enc_stages_operand(LPT)) {
     return hb_dyn_smem + threadIdx.x / TPI;        // staging area only (Mont::mul_sf), one warp per block
   } else if constexpr (M::HAS_SQR) {
     return hb_dyn_smem + threadIdx.x / TPI;        // one warp per block
@@ -121,7 +121,7 @@ struct EncArgs {
 };
 
 template <int LPT, int TPI>
-__global__ void __launch_bounds__(32, 4 * blocks_per_sm(LPT)) k_encrypt(EncArgs A) {
+__global__ void __launch_bounds__(32, 4 * enc_blocks_per_sm(LPT)) k_encrypt(EncArgs A) {
   using M = Mont<LPT, TPI>;
   constexpr int IPW = 32 / TPI;
   M mt;
