@@ -144,6 +144,29 @@ def main():
         pf = torch.empty((nw, wc), dtype=torch.int32, device="cuda")
         _native.check(lib.hb_powscalar(ctx.handle, c.data_ptr(), dkf.data_ptr(), pf.data_ptr(), nw, nw, 0, stream))
         checks["hmul_full_width"] = bool(np.array_equal(cpuref.powscalar_words(n, want_c[:nw].copy(), kfw), dev_u32(pf)))
+        # fused fore-gradient chain (arena.py:345-366 in one kernel) against its six-operator composition on the CPU:
+        # (1 + (lg kg mod n) n) r^n  *  c^kh  *  (1 + yl n), plain and resident operand / result forms
+        nf = min(count, 24000)
+        kg_int, kh = 4, 4
+        lg_ints = [int.from_bytes(row.tobytes(), "little") for row in m[:nf]]
+        glog = words([(v * kg_int) % n for v in lg_ints], wn)
+        yl = rand_words(n, wn, nf); yl[:len(adv_m)] = words(adv_m, wn)[:nf]
+        genc = cpuref.encrypt_words(n, glog, r[:nf].copy())
+        hpow = cpuref.powscalar_words(n, want_c[:nf].copy(), words([kh], wn))
+        ones = np.zeros((nf, wn), np.uint32); ones[:, 0] = 1
+        lifted = cpuref.encrypt_words(n, yl, ones)                       # (1 + yl n) * 1^n
+        want_f = cpuref.mulmod_words(n, cpuref.mulmod_words(n, genc, hpow), lifted)
+        dyl = torch.from_numpy(yl.view(np.int32)).cuda()
+        dkg = torch.from_numpy(words([kg_int], wn).view(np.int32)).cuda()
+        fo = torch.empty((nf, wc), dtype=torch.int32, device="cuda")
+        _native.check(lib.hb_fore_gradient(ctx.handle, c.data_ptr(), dm.data_ptr(), dkg.data_ptr(), kh, dyl.data_ptr(),
+                                           dr.data_ptr(), fo.data_ptr(), nf, 0, stream))
+        checks["fore_gradient"] = bool(np.array_equal(want_f, dev_u32(fo)))
+        fm = torch.empty((nf, lc), dtype=torch.int32, device="cuda")
+        _native.check(lib.hb_fore_gradient(ctx.handle, cm.data_ptr(), dm.data_ptr(), dkg.data_ptr(), kh, dyl.data_ptr(),
+                                           dr.data_ptr(), fm.data_ptr(), nf, A | O, stream))
+        _native.check(lib.hb_ct_convert(ctx.handle, fm.data_ptr(), fo.data_ptr(), nf, 0, stream))
+        checks["fore_gradient_resident"] = bool(np.array_equal(want_f, dev_u32(fo)))
         # hsum of everything
         one = torch.empty((1, wc), dtype=torch.int32, device="cuda")
         _native.check(lib.hb_product(ctx.handle, c.data_ptr(), one.data_ptr(), 1, count, 0, 1, stream))
