@@ -124,6 +124,18 @@ class CudaBackend(ExecutionBackend):
     # (lcm of 9472, 7104, 18944, 28416 instances per wave)
     STREAM_CHUNK = 56832
 
+    def _pinned_stage(self, tag: str, rows: int, wn: int):
+        """Page-locked int32 staging of at least rows x wn words, kept on the backend and only ever grown:
+        cudaHostAlloc of a few hundred MB costs tens of milliseconds, a streamed operator is called five times per
+        FLR iteration.  One operator runs at a time on a backend (callers are single-threaded)."""
+        t = device.torch()
+        stages = self.__dict__.setdefault("_stages", {})
+        need = rows * wn
+        buf = stages.get(tag)
+        if buf is None or buf.numel() < need:
+            buf = stages[tag] = t.empty((need + need // 8,), dtype=t.int32, pin_memory=True)
+        return buf[:need].view(rows, wn)
+
     def _draw_chunk(self, lib, n_words, wn, cnt, host_ptr, mt_state):
         """`cnt` values of randrange(1, n) into host memory: the MT19937 replay when mt_state = (state, index) is
         given, the operating system's CSPRNG otherwise."""
@@ -170,7 +182,7 @@ class CudaBackend(ExecutionBackend):
         n_words = device.ints_to_words([n], wn)
         chunk = self.STREAM_CHUNK
         nchunks = (count + chunk - 1) // chunk
-        pinned = [t.empty((chunk, wn), dtype=t.int32, pin_memory=True) for _ in range(2)]
+        pinned = self._pinned_stage("chunks", 2 * chunk, wn).view(2, chunk, wn)      # page-locking is slow to repeat
         staged = [t.empty((chunk, wn), dtype=t.int32, device="cuda") for _ in range(2)]
         copied = [None, None]
         checks = t.empty((nchunks, wc), dtype=t.int32, device="cuda")
@@ -814,7 +826,7 @@ class MultiDeviceBackend(CudaBackend):
         saved, mt_state = self._mt_state(rng)
         n_words = device.ints_to_words([n], wn)
         chunk = self.STREAM_CHUNK
-        pinned = t.empty((count, wn), dtype=t.int32, pin_memory=True)     # the whole draw, page-locked
+        pinned = self._pinned_stage("whole", count, wn)                   # the whole draw, page-locked (kept, grow-only)
         host = pinned.numpy()
 
         def run_chunk(be, lo, a, b, state):
