@@ -84,10 +84,16 @@ def respawn_under_torchrun(args) -> int:
     return subprocess.call(cmd)
 
 
-def bench_key():
-    """keygen(2048, default_rng(7)) -- the config-2 key."""
+def bench_key(product: bool = True):
+    """keygen(2048, default_rng(7)) -- the config-2 key -- as the checker's key object (p, q,
+    CRT constants).  The GPU arm takes it from the product's own key generation (host Python); the reference arm
+    from the oracle's, so that nothing of the product package is on its path.  Same seed, same key."""
     import hebatch_oracle as ho
-    return ho.keygen(KEY_BITS, random.Random(KEY_SEED))
+    if not product:
+        return ho.keygen(KEY_BITS, random.Random(KEY_SEED))
+    from paper_2107_13797_b200 import paillier
+    kp = paillier.keygen(KEY_BITS, paillier.default_rng(KEY_SEED))
+    return ho.Key(kp.public.n, kp.private.p, kp.private.q)
 
 
 class ClockSampler:
@@ -162,7 +168,7 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    key = bench_key()
+    key = bench_key(product=False)
     sample = args.cpu_sample
     for _ in range(args.warmup):
         cpu_reference_rate(key, max(64, sample // 16))
