@@ -361,22 +361,37 @@ class CompactScalars(WordArray):
             super().make_resident()
 
     def numpy(self) -> np.ndarray:
+        """Residues [rows * cols, wn] in row-major element order.  Negative scalars are n - magnitude: the low 64 bits
+        are a two-word subtraction, and its borrow runs up through n only while n's words are zero -- vectorised over
+        the elements, one pass per word the borrow actually reaches (normally one)."""
         if self._np is None:
-            mag = self.mag.cpu().numpy().view(np.uint64).reshape(self.cols, self.rows).T.reshape(-1)
-            neg = self.neg.cpu().numpy().reshape(self.cols, self.rows).T.reshape(-1).astype(bool)
-            out = np.zeros((self.count, self.width), np.uint32)
-            out[:, 0] = (mag & np.uint64(0xffffffff)).astype(np.uint32)
-            if self.width > 1:
-                out[:, 1] = (mag >> np.uint64(32)).astype(np.uint32)
-            if neg.any():                                         # residue of a negative scalar: n - magnitude
-                nw = ints_to_words([self.modulus], self.width)[0].astype(np.int64)
-                sub = out[neg].astype(np.int64)
-                borrow = np.zeros(sub.shape[0], np.int64)
-                for i in range(self.width):
-                    d = nw[i] - sub[:, i] - borrow
-                    borrow = (d < 0).astype(np.int64)
-                    sub[:, i] = d + (borrow << 32)
-                out[neg] = sub.astype(np.uint32)
+            mag = np.ascontiguousarray(self.mag.cpu().numpy().view(np.uint64).reshape(self.cols, self.rows).T).reshape(-1)
+            neg = np.ascontiguousarray(self.neg.cpu().numpy().reshape(self.cols, self.rows).T).reshape(-1).astype(bool)
+            width = self.width
+            out = np.zeros((self.count, width), np.uint32)
+            pos = ~neg
+            out[pos, 0] = (mag[pos] & np.uint64(0xffffffff)).astype(np.uint32)
+            if width > 1:
+                out[pos, 1] = (mag[pos] >> np.uint64(32)).astype(np.uint32)
+            if neg.any():
+                nw = ints_to_words([self.modulus], width)[0]
+                m = mag[neg]
+                n_lo = np.uint64(int(nw[0]) | ((int(nw[1]) << 32) if width > 1 else 0))
+                lo = n_lo - m                                      # wraps mod 2^64 exactly when a borrow leaves
+                res = np.broadcast_to(nw, (m.shape[0], width)).copy()
+                res[:, 0] = (lo & np.uint64(0xffffffff)).astype(np.uint32)
+                if width > 1:
+                    res[:, 1] = (lo >> np.uint64(32)).astype(np.uint32)
+                else:
+                    res[:, 0] = ((int(nw[0]) - m.astype(np.int64)) & 0xffffffff).astype(np.uint32)
+                borrow = np.nonzero(m > n_lo)[0]                   # rows whose subtraction borrows from word 2 up
+                i = 2
+                while borrow.size and i < width:
+                    word = res[borrow, i]
+                    res[borrow, i] = word - np.uint32(1)           # wraps to 0xffffffff when the word was zero
+                    borrow = borrow[word == 0]
+                    i += 1
+                out[neg] = res
             self._np = out
         return self._np
 
