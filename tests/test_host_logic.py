@@ -245,3 +245,26 @@ def test_native_draw_stream_equals_cpython_without_a_gpu():
         got = [int.from_bytes(r.tobytes(), "little") for r in out]
         assert all(1 <= v < n for v in got)
         assert n < 100 or len(set(got)) > count // 2
+
+
+def test_compact_scalars_materialise_the_reference_residues():
+    """device.CompactScalars.numpy(): sign + 64-bit magnitude, stored by column, back to the residues the reference
+    keeps (n - |k| for negatives) -- including moduli whose zero words make the borrow run (host logic, no GPU)."""
+    import random
+
+    import numpy as np
+    import torch
+    from paper_2107_13797_b200.device import CompactScalars
+    rng = random.Random(1)
+    for n in ((1 << 2047) + 12345, (1 << 127) + (1 << 70) + 5, rng.getrandbits(2048) | (1 << 2047) | 1,
+              (1 << 200) + 3, (1 << 255) + (1 << 64) + 1):
+        rows, cols = 31, 5
+        mags = [rng.getrandbits(rng.choice((1, 20, 52, 63, 64))) for _ in range(rows * cols)]
+        mags[:4] = [0, 1, 2 ** 64 - 1, 2 ** 63]
+        negs = [rng.random() < 0.5 and m != 0 for m in mags]
+        by_col = np.array(mags, dtype=np.uint64).reshape(rows, cols).T.reshape(-1).copy()
+        neg_col = np.array(negs, dtype=np.uint8).reshape(rows, cols).T.reshape(-1).copy()
+        cs = CompactScalars(n, rows, cols, torch.from_numpy(by_col.view(np.int64)), torch.from_numpy(neg_col), 64,
+                            int(sum(negs)))
+        got = [int.from_bytes(r.tobytes(), "little") for r in cs.numpy()]
+        assert got == [(n - m) % n if s else m for m, s in zip(mags, negs)]
